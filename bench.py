@@ -1,0 +1,408 @@
+"""Benchmark of the hot path: batched spline reconstruction on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+One JSON line on rank 0 (contract in the task statement).  A "step" is one
+evaluation of the configuration's full query batch (one kernel launch over
+N queries against a device-resident coset volume).  `value` is the whole-job
+reconstruction rate in G reconstructions/s (queries of all ranks / max-over-
+ranks device time); `e2e` is the same metric through the reference-facing C-ABI
+host call (`sg_eval_host`: H2D of the queries from pinned memory, kernel, D2H
+of the results, every step).
+
+Configs (BASELINE.json, restated concretely in SURVEY.md 8d):
+  c1  tricubic B-spline on Z^3, 64^3, 2^20 uniform queries
+  c2  BCC quintic box spline, 2 x 101^3 coset-split, 2^24 uniform queries  (default)
+Under torchrun every rank evaluates its own batch (weak scaling, volume replicated).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PROFILES = ROOT / "profiles"
+
+# name -> (space fixture, extents per coset, queries per GPU, query kind, grad)
+CONFIGS = {
+    "c1": dict(space="tricubic", extents=(64, 64, 64), queries=1 << 20, kind="uniform",
+               grad=False, desc="tensor-product tricubic B-spline on Z^3, 64^3, 2^20 uniform"),
+    "c2": dict(space="bcc_box5", extents=(101, 101, 101), queries=1 << 24, kind="uniform",
+               grad=False, desc="BCC quintic box spline (4 dirs x2), 2x101^3 coset-split, 2^24 uniform"),
+}
+DEFAULT_CONFIG = "c2"
+
+
+def _space_available(name):
+    from paper_2102_08518_b200.model import SPACES_DIR
+    return (SPACES_DIR / f"{name}.json").exists()
+
+
+def default_config_name():
+    return DEFAULT_CONFIG if _space_available(CONFIGS[DEFAULT_CONFIG]["space"]) else "c1"
+
+
+def gen_config_for(space, grad=False, **over):
+    from paper_2102_08518_b200 import GenConfig, ScheduleParams
+    n = space.stencil_size
+    kw = dict(params=ScheduleParams(1, n, "predicated"), float_width="f32",
+              unroll_cosets=space.ncosets == 1, form="horner", block=128, grad=grad)
+    kw.update(over)
+    return GenConfig(**kw)
+
+
+def build_program(cfg_name, **over):
+    from paper_2102_08518_b200 import generate, load_fixture
+    c = CONFIGS[cfg_name]
+    space = load_fixture(c["space"])
+    return space, generate(space, gen_config_for(space, c["grad"], **over), c["extents"])
+
+
+def precompile_bench_kernels():
+    from paper_2102_08518_b200.runtime import compile_source
+    for name, c in CONFIGS.items():
+        if _space_available(c["space"]):
+            _, prog = build_program(name)
+            compile_source(prog.source)
+
+
+def falg_per_query(space_name):
+    """Reference dynamic FP-op count (m=1, d=n, branchy), pinned by the golden script."""
+    p = ROOT / "tests" / "golden" / "falg.json"
+    d = json.loads(p.read_text()) if p.exists() else {}
+    return d.get(space_name)
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    d = json.loads(p.read_text()) if p.exists() else {}
+    sm_mhz = d.get("sm_max_mhz", 1965.0)
+    fp32 = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12   # TFLOP/s: SMs x FP32 lanes x FMA x clock
+    return dict(fp32_tflops=fp32, hbm_gbs=d.get("hbm_gbs", 6650.0), sm_max_mhz=sm_mhz,
+                source="MEASURED_PEAKS.json" if p.exists() else "fallback")
+
+
+# -- clocks ---------------------------------------------------------------------------
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50", "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# -- CPU baseline (oracle port; test-infrastructure import, baseline leg only) ---------------
+
+
+def _cpu_worker(args):
+    space_path, arrays, xs = args
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import refeval
+    sp = refeval.load_space_file(space_path)
+    t0 = time.perf_counter()
+    refeval.reference_eval_batch(sp, xs, arrays)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(space_name, arrays_f32, xs_f32, budget_s=15.0, shard=1 << 14):
+    """Time the oracle port (restatement of reference_eval_batch, numpy f64) on all
+    host cores over a bounded sample of the same workload."""
+    import multiprocessing as mp
+    from paper_2102_08518_b200.model import SPACES_DIR
+    path = str(SPACES_DIR / f"{space_name}.json")
+    arrays = [a.astype(np.float64) for a in arrays_f32]
+    cores = len(os.sched_getaffinity(0))
+    # calibrate on one shard
+    t1 = _cpu_worker((path, arrays, xs_f32[:shard].astype(np.float64)))
+    rate1 = shard / t1
+    nshards = max(cores, int(budget_s * rate1 * cores / shard) // cores * cores)
+    nshards = min(nshards, max(1, len(xs_f32) // shard))
+    jobs = [(path, arrays, xs_f32[i * shard:(i + 1) * shard].astype(np.float64))
+            for i in range(nshards)]
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(cores) as pool:
+        pool.map(_cpu_worker, jobs)
+    wall = time.perf_counter() - t0
+    n = nshards * shard
+    return {"value": n / wall / 1e9, "unit": "Grecon/s", "cores": cores, "kind": "port",
+            "sample": f"{n} of the configuration's queries ({nshards} shards of {shard}), "
+                      f"oracle/refeval.reference_eval_batch (numpy f64) on {cores} processes, "
+                      f"{wall:.1f}s; 1-core rate {rate1:.3e} q/s"}
+
+
+# -- workload ---------------------------------------------------------------------------
+
+
+def make_inputs(cfg_name, rank, device):
+    import torch
+    from paper_2102_08518_b200 import load_fixture
+    c = CONFIGS[cfg_name]
+    space = load_fixture(c["space"])
+    ext = c["extents"]
+    rng = np.random.default_rng(0)  # make_volume(seed=0): U[0,1), cosets in order
+    arrays = [rng.random(ext).astype(np.float32) for _ in range(space.ncosets)]
+    g = torch.Generator(device=device)
+    g.manual_seed(1 + rank)
+    spans = torch.tensor(ext, dtype=torch.float32, device=device)
+    xs = torch.rand((c["queries"], space.dim), generator=g, device=device) * spans
+    return space, arrays, xs
+
+
+def run_ours(args, rank, world, device):
+    import torch
+    import torch.distributed as dist
+    from paper_2102_08518_b200 import Evaluator
+    from paper_2102_08518_b200 import runtime
+
+    c = CONFIGS[args.config]
+    space, arrays, xs = make_inputs(args.config, rank, device)
+    _, prog = build_program(args.config)
+    # volume: rank 0's synthetic data broadcast over NCCL (replicated per GPU)
+    if world > 1:
+        dev_arrays = [torch.from_numpy(a).to(device) for a in arrays]
+        for t in dev_arrays:
+            dist.broadcast(t, 0)
+        ev = Evaluator(space, dev_arrays, prog=prog, device=device.index)
+    else:
+        ev = Evaluator(space, arrays, prog=prog, device=device.index)
+    n = xs.shape[0]
+    out = torch.empty(n, dtype=torch.float32, device=device)
+    stream = torch.cuda.current_stream(device)
+    l2_flush = None
+    if n * space.dim * 4 < 2 * 126e6:
+        l2_flush = torch.empty(int(256e6) // 4, dtype=torch.float32, device=device)
+
+    def step():
+        runtime.eval_device(ev.module, ev.volume, xs, out, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(device)
+    ev.module.status()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(device)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(device.index) as clk:
+        t_wall = time.perf_counter()
+        for i in range(args.steps):
+            if l2_flush is not None:
+                l2_flush.fill_(float(i))
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        torch.cuda.synchronize(device)
+        t_wall = time.perf_counter() - t_wall
+    if world > 1:
+        dist.barrier()
+    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    ev.module.status()
+    # max over ranks
+    tt = torch.tensor([ms], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms = float(tt.item())
+    total_q = n * world * args.steps
+    value = total_q / (ms / 1e3) / 1e9
+    kernel_ms = ms / args.steps
+
+    # ---- end to end through the C-ABI host path (pinned buffers)
+    xs_host = xs.cpu().pin_memory()
+    out_host = torch.empty(n, dtype=torch.float32).pin_memory()
+    e2e_steps = max(3, min(args.steps, 20))
+    lib = runtime.lib()
+
+    def host_step():
+        runtime._check(lib.sg_eval_host(ev.module.handle, ev.volume.handle,
+                                        runtime.ctypes.c_void_p(xs_host.data_ptr()), n,
+                                        runtime.ctypes.c_void_p(out_host.data_ptr()),
+                                        runtime.ctypes.c_void_p(0), 1 << 21))
+    host_step()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        host_step()
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = n * world * e2e_steps / float(te.item()) / 1e9
+    # correctness spot check of the timed kernel against the host path
+    ref_out = out[:4096].cpu()
+    assert torch.equal(ref_out, out_host[:4096]), "device and host paths disagree"
+
+    if rank != 0:
+        return None
+    pk = peaks()
+    falg = falg_per_query(c["space"])
+    roof = None
+    if falg:
+        achieved = falg * n / (kernel_ms / 1e3) / 1e12
+        traffic = None
+        tp = PROFILES / f"traffic_{args.config}.json"
+        if tp.exists():
+            traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
+        roof = {"bound": "fp32", "achieved": round(achieved, 3), "peak": round(pk["fp32_tflops"], 2),
+                "unit": "TFLOP/s", "frac": round(achieved / pk["fp32_tflops"], 4),
+                "traffic": traffic,
+                "note": f"F_alg = {falg:g} FP ops/query (reference dynamic count, m=1 d=n branchy; "
+                        f"tests/golden/falg.json); peak = 148 SM x 128 FP32 lanes x 2 x "
+                        f"{pk['sm_max_mhz']:.0f} MHz ({pk['source']} sm_max_mhz)"}
+    line = {
+        "metric": "G reconstructions/sec per B200 (fraction of FP32 roofline in roofline)",
+        "value": round(value, 4), "unit": "Grecon/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(kernel_ms, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": args.config + ": " + c["desc"], "space": c["space"],
+                   "extents": list(c["extents"]), "cosets": space.ncosets,
+                   "queries_per_gpu": n, "query_kind": c["kind"],
+                   "parallelism": f"query shards x{world}, volume replicated",
+                   "l2": "L2 flushed between steps" if l2_flush is not None
+                   else "query stream > L2 (126 MB); volume L2-resident by design"},
+        "e2e": {"value": round(e2e_value, 4), "unit": "Grecon/s",
+                "h2d_bytes_per_step": n * space.dim * 4, "d2h_bytes_per_step": n * 4,
+                "steps": e2e_steps},
+        "gpu_launches": args.steps,
+        "roofline": roof,
+        "clocks": clk.summary(),
+        "kernel": {"regs": ev.module.regs()[0], "fetch_mode": prog.meta["fetch_mode"],
+                   "form": prog.config.form, "wall_s": round(t_wall, 3)},
+    }
+    if not args.no_cpu:
+        xs_np = xs[: 1 << 20].cpu().numpy()
+        line["cpu_baseline"] = cpu_baseline(c["space"], arrays, xs_np, budget_s=args.cpu_budget)
+    return line
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU evaluator (oracle port) on all host cores."""
+    if rank != 0:
+        return None
+    from paper_2102_08518_b200 import load_fixture
+    c = CONFIGS[args.config]
+    space = load_fixture(c["space"])
+    rng = np.random.default_rng(0)
+    arrays = [rng.random(c["extents"]).astype(np.float32) for _ in range(space.ncosets)]
+    xs = (np.random.default_rng(1).random((1 << 20, space.dim)) *
+          np.array(c["extents"])).astype(np.float32)
+    per_step = max(5.0, 60.0 / max(1, args.steps + args.warmup))
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_baseline(c["space"], arrays, xs, budget_s=per_step)
+        if i >= args.warmup:
+            vals.append(r)
+    v = statistics.median([r["value"] for r in vals])
+    return {
+        "impl": "reference", "metric": "G reconstructions/sec per B200 (fraction of FP32 roofline in roofline)",
+        "value": v, "unit": "Grecon/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": args.config + ": " + c["desc"], "space": c["space"],
+                   "extents": list(c["extents"])},
+        "cpu_baseline": {**vals[-1], "value": v},
+        "e2e": {"value": v, "unit": "Grecon/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default=None)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    args.config = args.config or default_config_name()
+    args.warmup = max(3, args.warmup)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+        if line:
+            print(json.dumps(line), flush=True)
+        return 0
+    import torch
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=device)
+    line = run_ours(args, rank, world, device)
+    if line:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    raise SystemExit(main())

@@ -1,0 +1,122 @@
+/*
+ * splinegpu.h -- C ABI of the B200 (sm_100a) spline-reconstruction evaluator.
+ *
+ * This is the drop-in boundary for the reference's native execution path:
+ * the reference lowers a spline space to LLVM IR, builds it with clang and calls
+ *
+ *     T reconstruct(T x0, ..., T x{s-1},
+ *                   T* coset0, i64 ext0_0 ... ext0_{s-1}, ..., T* coset{M-1}, ...)
+ *
+ * once per query point through ctypes (reference pkg/src/splinegen/emit.py:237-241,
+ * argtypes pkg/src/splinegen/bench.py:239-247, per-point loop bench.py:259-263).
+ * Here the same computation is one batched, asynchronous launch over N points:
+ *
+ *   sg_compile        replaces `clang -O2 -shared kernel.ll` (bench.py:221-247): NVRTC
+ *                     compiles the generated CUDA source for sm_100a to a cubin.
+ *   sg_module_load    replaces ctypes.CDLL(kernel.so).reconstruct (bench.py:238).
+ *   sg_volume_create  replaces the per-call (pointer, extents) pairs (bench.py:253-258):
+ *                     coset arrays in the reference's C order (`DataVolume`,
+ *                     ir.py:524-558) are uploaded once, with a periodic ghost halo, so
+ *                     the per-fetch `srem` wrap of emit.py:186-212 happens once per coset.
+ *   sg_eval           replaces the per-point `fn(*row, *fixed)` loop (bench.py:259-263):
+ *                     xs is (N, s) row-major like `interpret_batch`'s input (ir.py:582).
+ *   sg_eval_host      the same with HOST buffers: H2D, kernel and D2H pipelined over
+ *                     chunks on internal streams (the end-to-end user call).
+ *   sg_module_status  reads/clears the device error word; SG_EUNREACHABLE mirrors the
+ *                     reference's sigma == -1 errors (ir.py:757-766, oracle.py:69-73),
+ *                     which the LLVM path leaves undefined (emit.py:161-164).
+ *
+ * Ownership: the caller owns xs/out/grad/dbg (device pointers for sg_eval, host
+ * pointers for sg_eval_host); the library owns modules and volumes.  All calls are
+ * thread-safe per (module, stream); the only global mutable state is the
+ * thread-local error string.  Every entry point returns an SG_* status.
+ */
+#ifndef SPLINEGPU_H
+#define SPLINEGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SG_OK = 0,
+  SG_EINVAL = 1,        /* shape / dtype / coset-count mismatch (ir.py:591-596) */
+  SG_ECUDA = 2,         /* CUDA runtime error (message in sg_last_error) */
+  SG_EUNREACHABLE = 3,  /* a point hit a sigma entry marked -1 */
+  SG_ECOMPILE = 4,      /* NVRTC compilation failed (log in sg_last_error) */
+  SG_ENOMEM = 5
+};
+
+enum { SG_F32 = 0, SG_F64 = 1 };
+
+#define SG_MAX_COSETS 8
+#define SG_MAX_DIM 4
+
+typedef struct sg_module sg_module;
+typedef struct sg_volume sg_volume;
+
+/* Static description of a generated kernel, filled in by the code generator. */
+typedef struct sg_module_info {
+  int32_t dim;                 /* s, 1..4 */
+  int32_t ncosets;             /* M, 1..SG_MAX_COSETS */
+  int32_t dtype;               /* SG_F32 | SG_F64: volume, query and output type */
+  int32_t block;               /* threads per CTA */
+  int32_t has_grad;            /* kernel writes grad (N, s) */
+  int32_t has_dbg;             /* kernel writes dbg (N, M, s+1): k then sub-region */
+  int32_t halo;                /* ghost-halo width the kernel's fetch offsets assume */
+  int32_t queries_per_thread;  /* >= 1 */
+  int64_t padded_extents[SG_MAX_COSETS][SG_MAX_DIM]; /* per coset, E + 2*halo */
+} sg_module_info;
+
+int sg_version(void);
+const char* sg_last_error(void);
+int sg_device_count(int* count);
+
+/* NVRTC: CUDA C++ source -> cubin for sm_100a.  *image is malloc'ed by the library
+ * (release with sg_free).  opts may be NULL.  On SG_ECOMPILE the log is in
+ * sg_last_error(). */
+int sg_compile(const char* source, const char* name, const char* const* opts, int nopts,
+               void** image, size_t* image_len, char** log);
+void sg_free(void* p);
+
+int sg_module_load(const void* image, size_t image_len, const char* entry, int device,
+                   const sg_module_info* info, sg_module** out);
+int sg_module_free(sg_module* m);
+int sg_module_regs(const sg_module* m, int* regs_per_thread, int* local_bytes);
+/* Reads the device error word (after synchronizing `stream`) and clears it.
+ * Returns SG_EUNREACHABLE if any point hit sigma == -1 since the last call. */
+int sg_module_status(sg_module* m, void* stream, uint32_t* flags);
+
+/* extents: ncosets x dim (row-major); src[c] points to coset c's C-order array of
+ * prod(extents[c]) elements, in HOST memory (src_on_device == 0) or device memory. */
+int sg_volume_create(int device, int dim, int ncosets, const int64_t* extents, int halo,
+                     int dtype, const void* const* src, int src_on_device, void* stream,
+                     sg_volume** out);
+int sg_volume_free(sg_volume* v);
+int sg_volume_bytes(const sg_volume* v, int64_t* bytes);
+/* Device address of coset c's padded array origin (for tests / peer copies). */
+int sg_volume_coset_ptr(const sg_volume* v, int coset, void** ptr);
+
+/* Asynchronous batched evaluation on `stream` (cudaStream_t; NULL = legacy default).
+ * xs: n x dim row-major (device), out: n (device), grad: n x dim or NULL,
+ * dbg: n x ncosets x (dim+1) int32 or NULL (required iff the module has_dbg). */
+int sg_eval(sg_module* m, const sg_volume* v, const void* xs, int64_t n, void* out,
+            void* grad, int32_t* dbg, void* stream);
+
+/* End-to-end evaluation with HOST buffers: the library pipelines H2D(xs chunk),
+ * kernel, D2H(out chunk) over `chunk` points per stage (0 = default) on its own
+ * streams and returns after the results are on the host.  Pinned host memory is
+ * recommended for full PCIe / C2C bandwidth. */
+int sg_eval_host(sg_module* m, const sg_volume* v, const void* xs_host, int64_t n,
+                 void* out_host, void* grad_host, int64_t chunk);
+
+/* Replicate a volume onto other devices (peer copy over NVLink when available). */
+int sg_volume_replicate(const sg_volume* v, int device, void* stream, sg_volume** out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPLINEGPU_H */

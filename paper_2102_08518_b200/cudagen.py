@@ -1,0 +1,770 @@
+"""CUDA C++ emission: spline space + variant knobs -> one sm_100a kernel.
+
+This replaces the reference's lowering + LLVM emission
+(pkg/src/splinegen/codegen.py:85-510 -> emit.py:43-262).  The generated kernel
+evaluates Algorithm 1 for ONE query per thread:
+
+  per coset l (unrolled, or a rolled loop -- codegen.py:406-469):
+    xl  = x - offset_l                                 (fp64)
+    k   = rnd(B^-1 xl) mapped back by B; x_loc = xl - k  (fp64, codegen.py:190-226)
+    q   = sum_i [normal_i . x_loc >= offset_i] << i      (fp64, codegen.py:230-250)
+    sub = sigma[q mod p]; sigma == -1 sets the error word
+    u   = T_sub x_loc + t'_sub                          (codegen.py:281-304)
+    c_j = V_l[wrap(k) + pi_sub[j]]  (ghost halo: one wrap per coset, not per fetch)
+    g   = psi_{psi(sub)}(u, c)  via the scheduled chunk trees  (codegen.py:332-402)
+  f = sum_l g_l
+
+Selection (rho, plane tests) runs in fp64 op-for-op like the fp64 oracle
+(oracle.py:34-74), which makes k and the sub-region bit-exact against it
+(SURVEY H2); polynomial evaluation runs in the program dtype (f32 or f64).
+
+Variant knobs (GenConfig): the reference's (m, d, branch_mode, refetch_tables,
+float_width, unroll_cosets) plus GPU ones -- `form` ("horner": the reference's
+greedy Horner trees per chunk; "sites": per-site weight polynomials
+w_j(u) = d psi / d c_j in Horner form, then sum c_j w_j), `coeffs` ("imm":
+hard-coded FMA immediates; "lut": coefficients in a __constant__ lookup table
+read as constant-bank operands), `block`, `grad`, `dbg`.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import struct
+from dataclasses import dataclass, field, replace
+from fractions import Fraction
+
+import numpy as np
+
+from . import exact
+from .model import PARALLELEPIPED, ROUND_NEAREST, SplineSpace, validate_space
+from .poly import NO_SYMBOL, Add, Const, Mul, Poly, Sym, Var, group_polynomial, horner_factorize
+from .schedule import BRANCHY, COMPUTE, FETCH, PREDICATED, ScheduleParams, schedule_pipeline
+
+F64 = "f64"
+F32 = "f32"
+ENTRY = "sg_eval_kernel"
+FORMS = ("horner", "sites")
+COEFFS = ("imm", "lut")
+
+
+@dataclass(frozen=True)
+class GenConfig:
+    """Reference fields (codegen.py:38-46) + B200 kernel-variant knobs."""
+    params: ScheduleParams
+    float_width: str = F32
+    unroll_cosets: bool = True
+    form: str = "horner"
+    coeffs: str = "imm"
+    block: int = 128
+    grad: bool = False
+    dbg: bool = False
+    min_blocks: int = 0          # __launch_bounds__ second argument (0 = let ptxas pick)
+
+    def __post_init__(self):
+        if self.float_width not in (F64, F32):
+            raise ValueError(f"float width must be f64 or f32, not {self.float_width!r}")
+        if self.form not in FORMS:
+            raise ValueError(f"form must be one of {FORMS}")
+        if self.coeffs not in COEFFS:
+            raise ValueError(f"coeffs must be one of {COEFFS}")
+        if self.block % 32 or not 32 <= self.block <= 1024:
+            raise ValueError("block must be a multiple of 32 in [32, 1024]")
+
+
+def default_config(space: SplineSpace, **kw) -> GenConfig:
+    """The paper's GPU default: m = 1, d = n, predicated."""
+    n = space.stencil_size
+    params = kw.pop("params", None) or ScheduleParams(1, n, PREDICATED)
+    return GenConfig(params=params, **kw)
+
+
+# -- literals ------------------------------------------------------------------
+
+
+def flit(q, fw: str) -> str:
+    """Exact hex literal of the rational rounded to the program float type."""
+    v = float(Fraction(q))
+    if fw == F32:
+        v32 = float(np.float32(v))
+        if v32 == 0.0:
+            return "0.0f"
+        return f"{v32.hex()}f"
+    if v == 0.0:
+        return "0.0"
+    return v.hex()
+
+
+def dlit(q) -> str:
+    v = float(Fraction(q))
+    return "0.0" if v == 0.0 else v.hex()
+
+
+# -- derived tables --------------------------------------------------------------
+
+
+@dataclass
+class Tables:
+    s: int
+    M: int
+    nsub: int
+    n: int
+    K: int
+    cosets: list            # M x s Fractions
+    planes: list            # (normal Fractions, offset Fraction)
+    modulus: int
+    sigma: list
+    compress: bool
+    transforms: list        # nsub x (s x s Fractions)
+    tshift: list            # nsub x s Fractions  (t' = -T t)
+    stencils: list          # nsub x n x s ints
+    psi: list               # nsub ints
+    halo: int
+    uniform_T: bool
+    uniform_tp: bool
+    uniform_stencil: bool
+    uniform_psi: bool
+    affine: list | None     # per sub: (A int s x s, b int s) with pi_sub[j] = A ref[j] + b
+    ref_stencil: list       # n x s
+
+
+def _solve_affine(ref, sten, s):
+    """Find integer A, b with sten[j] = A ref[j] + b for all j (or None)."""
+    n = len(ref)
+    if n == 0:
+        return None
+    # pick s independent difference vectors of ref
+    diffs = [(j, tuple(ref[j][d] - ref[0][d] for d in range(s))) for j in range(1, n)]
+    basis = []
+    for j, v in diffs:
+        cand = basis + [(j, v)]
+        m = [list(map(Fraction, w)) for _, w in cand]
+        # rank check via determinant of the Gram-like selection
+        if _rank(m) == len(cand):
+            basis = cand
+        if len(basis) == s:
+            break
+    if len(basis) < s:
+        # degenerate stencil (e.g. n <= s): only translations are tried
+        b = tuple(sten[0][d] - ref[0][d] for d in range(s))
+        A = exact.eye(s)
+        if all(tuple(ref[j][d] + b[d] for d in range(s)) == tuple(sten[j]) for j in range(n)):
+            return [[int(v) for v in row] for row in A], list(b)
+        return None
+    R = [[Fraction(v[d]) for (_, v) in basis] for d in range(s)]   # columns = ref diffs
+    S = [[Fraction(sten[j][d] - sten[0][d]) for (j, _) in basis] for d in range(s)]
+    try:
+        Rinv = exact.inverse(tuple(tuple(r) for r in R))
+    except ValueError:
+        return None
+    A = exact.matmul(tuple(tuple(r) for r in S), Rinv)
+    if not exact.is_int_mat(A):
+        return None
+    b = exact.sub(tuple(Fraction(v) for v in sten[0]), exact.matvec(A, ref[0]))
+    if not exact.is_int_vec(b):
+        return None
+    for j in range(n):
+        got = exact.add(exact.matvec(A, ref[j]), b)
+        if tuple(int(v) for v in got) != tuple(sten[j]):
+            return None
+    return [[int(v) for v in row] for row in A], [int(v) for v in b]
+
+
+def _rank(rows):
+    a = [list(r) for r in rows]
+    rank = 0
+    ncol = len(a[0]) if a else 0
+    for c in range(ncol):
+        p = next((r for r in range(rank, len(a)) if a[r][c] != 0), None)
+        if p is None:
+            continue
+        a[rank], a[p] = a[p], a[rank]
+        for r in range(len(a)):
+            if r != rank and a[r][c] != 0:
+                f = a[r][c] / a[rank][c]
+                a[r] = [x - f * y for x, y in zip(a[r], a[rank])]
+        rank += 1
+    return rank
+
+
+def derive_tables(space: SplineSpace) -> Tables:
+    s = space.dim
+    subs = space.subregions
+    transforms = [tuple(tuple(Fraction(v) for v in row) for row in sb.transform) for sb in subs]
+    tshift = [exact.neg(exact.matvec(sb.transform, sb.shift)) for sb in subs]
+    stencils = [[tuple(int(v) for v in site) for site in sb.stencil] for sb in subs]
+    psi = [sb.psi_index for sb in subs]
+    halo = max([abs(v) for st in stencils for site in st for v in site] + [0])
+    ref = stencils[0]
+    aff = []
+    for st in stencils:
+        r = _solve_affine(ref, st, s)
+        if r is None:
+            aff = None
+            break
+        aff.append(r)
+    P = space.indexer.modulus
+    Q = len(space.planes)
+    return Tables(
+        s=s, M=space.ncosets, nsub=len(subs), n=space.stencil_size, K=len(space.ref_polys),
+        cosets=[tuple(Fraction(v) for v in c) for c in space.lattice.cosets],
+        planes=[(tuple(Fraction(v) for v in p.normal), Fraction(p.offset)) for p in space.planes],
+        modulus=P, sigma=list(space.indexer.sigma), compress=(Q > 0 and 2 ** Q > P),
+        transforms=transforms, tshift=tshift, stencils=stencils, psi=psi, halo=halo,
+        uniform_T=len(set(transforms)) == 1, uniform_tp=len(set(tshift)) == 1,
+        uniform_stencil=len({tuple(x) for x in stencils}) == 1, uniform_psi=len(set(psi)) == 1,
+        affine=aff, ref_stencil=ref)
+
+
+# -- expression emission -------------------------------------------------------------
+
+
+class Emitter:
+    def __init__(self, fw: str):
+        self.fw = fw
+        self.T = "float" if fw == F32 else "double"
+        self.lines = []
+        self.nt = 0
+        self.indent = "  "
+
+    def tmp(self, prefix="t"):
+        self.nt += 1
+        return f"{prefix}{self.nt}"
+
+    def line(self, text):
+        self.lines.append(self.indent + text)
+
+    def tree(self, node, u, c, consts=None):
+        """Post-order emission of a Horner tree; returns the operand string."""
+        out = {}
+        stack = [(node, False)]
+        while stack:
+            nd, done = stack.pop()
+            key = id(nd)
+            if key in out:
+                continue
+            if isinstance(nd, Const):
+                out[key] = consts(nd.value) if consts else flit(nd.value, self.fw)
+            elif isinstance(nd, Var):
+                out[key] = u[nd.index]
+            elif isinstance(nd, Sym):
+                out[key] = c[nd.index]
+            elif not done:
+                stack.append((nd, True))
+                stack.append((nd.right, False))
+                stack.append((nd.left, False))
+            else:
+                a, b = out[id(nd.left)], out[id(nd.right)]
+                t = self.tmp()
+                op = "+" if isinstance(nd, Add) else "*"
+                self.line(f"const {self.T} {t} = {a} {op} {b};")
+                out[key] = t
+        return out[id(node)]
+
+
+# -- program ----------------------------------------------------------------------
+
+
+@dataclass
+class CudaProgram:
+    """A generated kernel: source + the metadata the C ABI needs."""
+    name: str
+    source: str
+    entry: str
+    dim: int
+    ncosets: int
+    float_width: str
+    block: int
+    halo: int
+    extents: tuple           # per coset (unpadded)
+    padded_extents: tuple
+    has_grad: bool
+    has_dbg: bool
+    config: GenConfig
+    space: SplineSpace = field(repr=False)
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def key(self) -> str:
+        return hashlib.sha256(self.source.encode()).hexdigest()[:24]
+
+    @property
+    def dtype(self):
+        return np.float32 if self.float_width == F32 else np.float64
+
+
+def _chunk_trees(space, cfg, t: Tables):
+    """Per reference polynomial: per chunk, the tree to evaluate (or None)."""
+    n = t.n
+    m = cfg.params.group_size
+    out = []
+    for rp in space.ref_polys:
+        cs = group_polynomial(rp.poly, m, range(n))
+        trees = []
+        for poly, block in cs.chunks:
+            if not poly:
+                trees.append(None)
+                continue
+            if cfg.form == "horner":
+                trees.append(horner_factorize(poly))
+            else:
+                node = None
+                free = Poly(poly.dim, {k: v for k, v in poly.terms.items() if k[1] == NO_SYMBOL})
+                if free:
+                    node = horner_factorize(free)
+                for j in block:
+                    w = poly.coefficient_of(j)
+                    if not w:
+                        continue
+                    term = Mul(horner_factorize(w), Sym(j))
+                    node = term if node is None else Add(node, term)
+                trees.append(node)
+        out.append(trees)
+    return out
+
+
+def _grad_trees(space, cfg, t: Tables):
+    """Per reference polynomial, per axis: one Horner tree of d psi / d u_axis."""
+    out = []
+    for rp in space.ref_polys:
+        per = []
+        for a in range(t.s):
+            dp = rp.poly.differentiate(a)
+            per.append(horner_factorize(dp) if dp else None)
+        out.append(per)
+    return out
+
+
+def generate(space, config: GenConfig | None = None, extents=None,
+             validate: bool = True) -> CudaProgram:
+    """Generate the CUDA kernel for `space` (reference `generate`, codegen.py:508).
+
+    `extents`: per-coset volume extents (tuple of s ints, or one tuple per coset);
+    the kernel is specialized on the padded strides so every fetch offset of a
+    uniform stencil is an immediate.  Defaults to 64 per axis.
+    """
+    if not isinstance(space, SplineSpace):
+        space = SplineSpace.adopt(space)
+    errors = [d for d in validate_space(space) if d.severity == "error"] if validate else []
+    if errors:
+        raise ValueError(f"space is not valid: {errors[0]}")
+    cfg = config or default_config(space)
+    t = derive_tables(space)
+    s, M = t.s, t.M
+    if extents is None:
+        extents = (64,) * s
+    ext = tuple(tuple(int(v) for v in e) for e in extents) if isinstance(extents[0], (tuple, list)) \
+        else tuple(tuple(int(v) for v in extents) for _ in range(M))
+    if len(ext) != M or any(len(e) != s for e in ext):
+        raise ValueError(f"extents must give {s} values for each of {M} cosets")
+    h = t.halo
+    pext = tuple(tuple(e + 2 * h for e in row) for row in ext)
+    for row in pext:
+        nel = 1
+        for e in row:
+            nel *= e
+        if nel >= 2 ** 31:
+            raise ValueError("coset array too large for 32-bit element offsets")
+    strides = []
+    for row in pext:
+        st = [1] * s
+        for d in range(s - 2, -1, -1):
+            st[d] = st[d + 1] * row[d + 1]
+        strides.append(st)
+    same_geom = len(set(pext)) == 1
+
+    fw = cfg.float_width
+    em = Emitter(fw)
+    T = em.T
+    P = t.modulus
+    trees = _chunk_trees(space, cfg, t)
+    gtrees = _grad_trees(space, cfg, t) if cfg.grad else None
+    plans = [schedule_pipeline(group_polynomial(space.ref_polys[sb.psi_index].poly,
+                                                cfg.params.group_size, range(t.n)), cfg.params)
+             for sb in space.subregions]
+    plan = plans[0]
+    assert all(p.steps == plan.steps for p in plans), "plans differ across sub-regions"
+    refetch = cfg.params.refetch_tables
+
+    head = []
+    A = head.append
+    A(f"// generated by paper_2102_08518_b200.cudagen for space '{space.name}'")
+    A(f"// m={cfg.params.group_size} d={cfg.params.pipeline_depth} mode={cfg.params.branch_mode} "
+      f"refetch={str(refetch).lower()} unroll_cosets={str(cfg.unroll_cosets).lower()} "
+      f"form={cfg.form} coeffs={cfg.coeffs} {fw} block={cfg.block} grad={int(cfg.grad)} "
+      f"dbg={int(cfg.dbg)}")
+    A(f"// extents={ext} halo={h}")
+    A("struct SgCosets { const void* base[8]; };")
+
+    # ---- tables ------------------------------------------------------------
+    smem = []     # (name, ctype, values)
+    use_sigma = t.nsub > 1 and len(space.planes) > 0 and len(set(t.sigma)) > 1
+    if use_sigma:
+        smem.append(("sg_sigma", "int", list(t.sigma)))
+    if not t.uniform_T:
+        smem.append(("sg_T", T, [float(v) for tr in t.transforms for row in tr for v in row]))
+    if not t.uniform_tp:
+        smem.append(("sg_tp", T, [float(v) for tp in t.tshift for v in tp]))
+    fetch_mode = "uniform" if t.uniform_stencil else ("affine" if t.affine is not None else "table")
+    if fetch_mode != "uniform" and not same_geom and not cfg.unroll_cosets:
+        pass  # per-coset strides are compile-time constants in unrolled mode only; handled below
+    if fetch_mode == "affine":
+        # per geometry g: S'_sub = A_sub^T S (s ints) and boff_sub = b_sub . S
+        for g, st in enumerate(strides if not same_geom else strides[:1]):
+            vals = []
+            for A_, b_ in t.affine:
+                sp = [sum(A_[d][e] * st[d] for d in range(s)) for e in range(s)]
+                vals += sp + [sum(b_[d] * st[d] for d in range(s))]
+            smem.append((f"sg_aff{g}", "int", vals))
+    elif fetch_mode == "table":
+        npad = t.n + 1 if t.n % 2 == 0 else t.n
+        for g, st in enumerate(strides if not same_geom else strides[:1]):
+            vals = []
+            for sten in t.stencils:
+                row = [sum(site[d] * st[d] for d in range(s)) for site in sten]
+                vals += row + [0] * (npad - t.n)
+            smem.append((f"sg_off{g}", "int", vals))
+    if not t.uniform_psi and t.K > 1:
+        smem.append(("sg_psi", "int", list(t.psi)))
+
+    lut = []
+    if cfg.coeffs == "lut":
+        lut_index = {}
+
+        def lut_const(q):
+            v = float(np.float32(float(q))) if fw == F32 else float(q)
+            if v not in lut_index:
+                lut_index[v] = len(lut)
+                lut.append(v)
+            return f"sg_lut[{lut_index[v]}]"
+        consts = lut_const
+    else:
+        consts = None
+
+    for name, ctype, vals in smem:
+        lit = ", ".join(repr(v) if ctype != "int" else str(v) for v in vals)
+        if ctype == "float":
+            lit = ", ".join(flit(Fraction(v), F32) for v in vals)
+        elif ctype == "double":
+            lit = ", ".join(dlit(Fraction(v)) for v in vals)
+        A(f"__constant__ {ctype} {name}_c[{len(vals)}] = {{{lit}}};")
+
+    # ---- kernel -------------------------------------------------------------
+    lb = f"{cfg.block}, {cfg.min_blocks}" if cfg.min_blocks else f"{cfg.block}"
+    body = []
+    B = body.append
+    B(f'extern "C" __global__ void __launch_bounds__({lb}) {ENTRY}(')
+    B(f"    const {T}* __restrict__ xs, long long n, {T}* __restrict__ out, {T}* __restrict__ grad,")
+    B("    int* __restrict__ dbg, unsigned* __restrict__ err, SgCosets vol) {")
+    for name, ctype, vals in smem:
+        B(f"  __shared__ {ctype} {name}[{len(vals)}];")
+    for name, ctype, vals in smem:
+        B(f"  for (int i_ = threadIdx.x; i_ < {len(vals)}; i_ += {cfg.block}) {name}[i_] = {name}_c[i_];")
+    if smem:
+        B("  __syncthreads();")
+    B(f"  const long long qi = (long long)blockIdx.x * {cfg.block} + threadIdx.x;")
+    B("  if (qi >= n) return;")
+    for d in range(s):
+        B(f"  const double x{d} = (double)xs[qi * {s} + {d}];")
+    B(f"  {T} acc = ({T})0;")
+    if cfg.grad:
+        for d in range(s):
+            B(f"  {T} gacc{d} = ({T})0;")
+    em.lines = []
+
+    def emit_coset(l, dyn):
+        """Body for coset `l` (int) or the loop variable `l` (dyn=True)."""
+        L = em.line
+        if dyn:
+            ptr = f"(const {T}*)vol.base[0]"
+            for c in range(1, M):
+                ptr = f"(l == {c} ? (const {T}*)vol.base[{c}] : {ptr})"
+            L(f"const {T}* __restrict__ V = {ptr};")
+            for d in range(s):
+                offs = [float(t.cosets[c][d]) for c in range(M)]
+                if all(o == 0.0 for o in offs):
+                    L(f"const double xl{d} = x{d};")
+                else:
+                    expr = dlit(t.cosets[0][d])
+                    for c in range(1, M):
+                        expr = f"(l == {c} ? {dlit(t.cosets[c][d])} : {expr})"
+                    L(f"const double xl{d} = __dsub_rn(x{d}, {expr});")
+        else:
+            L(f"const {T}* __restrict__ V = (const {T}*)vol.base[{l}];")
+            for d in range(s):
+                o = t.cosets[l][d]
+                if o == 0:
+                    L(f"const double xl{d} = x{d};")
+                else:
+                    L(f"const double xl{d} = __dsub_rn(x{d}, {dlit(o)});")
+        # ---- rho (codegen.py:190-226, oracle.py:38-53)
+        rm = space.region_map
+        if rm.shape == PARALLELEPIPED:
+            basis, rounding = rm.basis, rm.rounding
+        else:
+            basis, rounding = exact.eye(s), ROUND_NEAREST
+
+        def rnd(v):
+            if rounding == ROUND_NEAREST:
+                return (f"(({v}) >= 0.0 ? floor(__dadd_rn(({v}), 0.5)) : "
+                        f"ceil(__dsub_rn(({v}), 0.5)))")
+            return f"floor({v})"
+        if exact.is_identity(basis):
+            for d in range(s):
+                L(f"const long long k{d} = (long long){rnd(f'xl{d}')};")
+        else:
+            inv = exact.inverse(basis)
+            for d in range(s):
+                acc = None
+                for e in range(s):
+                    if inv[d][e] == 0:
+                        continue
+                    term = f"xl{e}" if inv[d][e] == 1 else f"__dmul_rn(xl{e}, {dlit(inv[d][e])})"
+                    acc = term if acc is None else f"__dadd_rn({acc}, {term})"
+                L(f"const double bu{d} = {acc or '0.0'};")
+                L(f"const long long r{d} = (long long){rnd(f'bu{d}')};")
+            for d in range(s):
+                terms = [f"{int(basis[d][e])}LL * r{e}" for e in range(s) if basis[d][e] != 0]
+                L(f"const long long k{d} = {' + '.join(terms) or '0LL'};")
+        for d in range(s):
+            L(f"const double xc{d} = __dsub_rn(xl{d}, (double)k{d});")
+        # ---- membership (codegen.py:230-250; oracle dot = left-to-right)
+        if space.planes:
+            L("unsigned q = 0u;")
+            for i, (nrm, off) in enumerate(t.planes):
+                acc = None
+                for e in range(s):
+                    w = nrm[e]
+                    if w == 0:
+                        continue
+                    term = f"xc{e}" if w == 1 else (f"(-xc{e})" if w == -1
+                                                      else f"__dmul_rn(xc{e}, {dlit(w)})")
+                    acc = term if acc is None else f"__dadd_rn({acc}, {term})"
+                L(f"q |= (({acc or '0.0'}) >= {dlit(off)}) ? {1 << i}u : 0u;")
+            if t.compress:
+                L(f"q = q % {P}u;")
+            if use_sigma:
+                L("int sub = sg_sigma[q];")
+            else:
+                v = t.sigma[0] if t.sigma else 0
+                L(f"int sub = {v};")
+                if any(x < 0 for x in t.sigma):
+                    pass
+            if any(x < 0 for x in t.sigma):
+                if use_sigma:
+                    L("if (sub < 0) { atomicOr(err, 1u); sub = 0; }")
+                else:
+                    bad = [qq for qq, x in enumerate(t.sigma) if x < 0]
+                    cond = " || ".join(f"q == {qq}u" for qq in bad)
+                    L(f"if ({cond}) atomicOr(err, 1u);")
+        else:
+            L("const int sub = 0;")
+        if cfg.dbg:
+            cols = s + 1
+            base = f"(qi * {M} + {l}) * {cols}" if not dyn else f"(qi * {M} + l) * {cols}"
+            for d in range(s):
+                L(f"dbg[{base} + {d}] = (int)k{d};")
+            L(f"dbg[{base} + {s}] = sub;")
+        # ---- wrap k once per coset, flat base index in the padded array
+        geo = 0 if (same_geom or dyn) else l
+        if not same_geom and dyn:
+            raise ValueError("rolled coset loop needs equal coset extents")
+        e_ = ext[geo]
+        st_ = strides[geo]
+        for d in range(s):
+            L(f"int kw{d} = (int)k{d};")
+            L(f"if ((unsigned)kw{d} >= {e_[d]}u) {{ long long m_ = k{d} % {e_[d]}LL; "
+              f"kw{d} = (int)(m_ < 0 ? m_ + {e_[d]}LL : m_); }}")
+        L("const int base = " + " + ".join(
+            f"kw{d} * {st_[d]}" if st_[d] != 1 else f"kw{d}" for d in range(s)) + ";")
+        # ---- per-sub fetch offsets
+        if fetch_mode == "affine":
+            gi = 0 if same_geom else geo
+            L(f"const int* aff = &sg_aff{gi}[sub * {s + 1}];")
+            for e in range(s):
+                L(f"const int sp{e} = aff[{e}];")
+            L(f"const int boff = base + aff[{s}];")
+            vals = {e: sorted({site[e] for site in t.ref_stencil}) for e in range(s)}
+            for e in range(s):
+                for v in vals[e]:
+                    if v == 0:
+                        continue
+                    name = f"mp{e}_{v}" if v > 0 else f"mn{e}_{-v}"
+                    L(f"const int {name} = {v} * sp{e};")
+
+            def off_expr(j):
+                site = t.ref_stencil[j]
+                parts = ["boff"]
+                for e in range(s):
+                    v = site[e]
+                    if v:
+                        parts.append(f"mp{e}_{v}" if v > 0 else f"mn{e}_{-v}")
+                return " + ".join(parts)
+        elif fetch_mode == "table":
+            gi = 0 if same_geom else geo
+            npad = t.n + 1 if t.n % 2 == 0 else t.n
+            L(f"const int* offt = &sg_off{gi}[sub * {npad}];")
+
+            def off_expr(j):
+                return f"base + offt[{j}]"
+        else:
+            sten = t.stencils[0]
+
+            def off_expr(j):
+                o = sum(sten[j][d] * st_[d] for d in range(s))
+                return f"base + ({o})" if o else "base"
+        # ---- local point u = T x_loc + t'
+        for d in range(s):
+            L(f"const {T} xf{d} = ({T})xc{d};")
+
+        def emit_u(tag):
+            us = []
+            for d in range(s):
+                if t.uniform_T:
+                    row = t.transforms[0][d]
+                    acc = None
+                    for e in range(s):
+                        w = row[e]
+                        if w == 0:
+                            continue
+                        term = f"xf{e}" if w == 1 else (f"(-xf{e})" if w == -1
+                                                         else f"{flit(w, fw)} * xf{e}")
+                        acc = term if acc is None else f"{acc} + {term}"
+                    acc = acc or f"({T})0"
+                else:
+                    acc = " + ".join(f"sg_T[sub * {s * s} + {d * s + e}] * xf{e}" for e in range(s))
+                if t.uniform_tp:
+                    tp = t.tshift[0][d]
+                    if tp != 0:
+                        acc = f"{acc} + {flit(tp, fw)}"
+                else:
+                    acc = f"{acc} + sg_tp[sub * {s} + {d}]"
+                name = f"u{d}{tag}"
+                L(f"const {T} {name} = {acc};")
+                us.append(name)
+            return us
+
+        # ---- fetch + compute following the (m, d) plan
+        if t.K > 1:
+            if t.uniform_psi:
+                L(f"const int psi = {t.psi[0]};")
+            else:
+                L("const int psi = sg_psi[sub];")
+        cvars = [f"c{j}" for j in range(t.n)]
+
+        def run_plan(psis, tag):
+            accs = {i: None for i in psis}
+            u = None
+            nchunk = 0
+            for step in plan.steps:
+                if step.kind == FETCH:
+                    j = step.index
+                    L(f"const {T} c{j}{tag} = __ldg(V + ({off_expr(j)}));")
+                elif step.kind == COMPUTE:
+                    if u is None or refetch:
+                        u = emit_u(f"{tag}_{nchunk}" if refetch else tag)
+                    for i in psis:
+                        tree = trees[i][step.index]
+                        if tree is None:
+                            continue
+                        cv = [f"{c}{tag}" for c in cvars]
+                        v = em.tree(tree, u, cv, consts)
+                        if accs[i] is None:
+                            accs[i] = v
+                        else:
+                            nt = em.tmp("a")
+                            L(f"const {T} {nt} = {accs[i]} + {v};")
+                            accs[i] = nt
+                    nchunk += 1
+            grads = None
+            if cfg.grad:
+                grads = {}
+                for i in psis:
+                    cv = [f"{c}{tag}" for c in cvars]
+                    du = []
+                    for a in range(s):
+                        tr = gtrees[i][a]
+                        du.append(em.tree(tr, u, cv, consts) if tr is not None else f"({T})0")
+                    grads[i] = du
+            return {i: (v if v is not None else f"({T})0") for i, v in accs.items()}, grads, u
+
+        def add_grad(du, tr_known):
+            # grad_x += T^T du  (T = sub transform)
+            for e in range(s):
+                parts = []
+                for a in range(s):
+                    if t.uniform_T:
+                        w = t.transforms[0][a][e]
+                        if w == 0:
+                            continue
+                        parts.append(du[a] if w == 1 else (f"(-{du[a]})" if w == -1
+                                                           else f"{flit(w, fw)} * {du[a]}"))
+                    else:
+                        parts.append(f"sg_T[sub * {s * s} + {a * s + e}] * {du[a]}")
+                if parts:
+                    L(f"gacc{e} += {' + '.join(parts)};")
+
+        if t.K == 1:
+            accs, grads, _ = run_plan([0], "")
+            L(f"acc += {accs[0]};")
+            if cfg.grad:
+                add_grad(grads[0], True)
+        elif cfg.params.branch_mode == PREDICATED:
+            accs, grads, _ = run_plan(list(range(t.K)), "")
+            sel = " + ".join(f"(psi == {i} ? {accs[i]} : ({T})0)" for i in range(t.K))
+            L(f"acc += {sel};")
+            if cfg.grad:
+                du = []
+                for a in range(s):
+                    du.append(em.tmp("gd"))
+                    L(f"const {T} {du[-1]} = " + " + ".join(
+                        f"(psi == {i} ? {grads[i][a]} : ({T})0)" for i in range(t.K)) + ";")
+                add_grad(du, True)
+        else:  # branchy: compare chain, one arm per reference polynomial
+            for i in range(t.K):
+                kw = "if" if i == 0 else "} else if"
+                cond = f"psi == {i}" if i < t.K - 1 else "true"
+                L(f"{kw} ({cond}) {{" if i < t.K - 1 else "} else {")
+                em.indent += "  "
+                accs, grads, _ = run_plan([i], f"_{i}")
+                L(f"acc += {accs[i]};")
+                if cfg.grad:
+                    add_grad(grads[i], True)
+                em.indent = em.indent[:-2]
+            L("}")
+
+    if M == 1:
+        em.line("{")
+        em.indent = "    "
+        emit_coset(0, False)
+        em.indent = "  "
+        em.line("}")
+    elif cfg.unroll_cosets:
+        for l in range(M):
+            em.line(f"{{  // coset {l}")
+            em.indent = "    "
+            emit_coset(l, False)
+            em.indent = "  "
+            em.line("}")
+    else:
+        em.line("#pragma unroll 1")
+        em.line(f"for (int l = 0; l < {M}; ++l) {{")
+        em.indent = "    "
+        emit_coset(None, True)
+        em.indent = "  "
+        em.line("}")
+    body += em.lines
+    body.append("  out[qi] = acc;")
+    if cfg.grad:
+        for d in range(s):
+            body.append(f"  grad[qi * {s} + {d}] = gacc{d};")
+    body.append("}")
+    if lut:
+        lit = ", ".join(flit(Fraction(v), fw) for v in lut)
+        head.append(f"__constant__ {T} sg_lut[{len(lut)}] = {{{lit}}};")
+    src = "\n".join(head + body) + "\n"
+    return CudaProgram(
+        name=space.name, source=src, entry=ENTRY, dim=s, ncosets=M, float_width=fw,
+        block=cfg.block, halo=h, extents=ext, padded_extents=pext, has_grad=cfg.grad,
+        has_dbg=cfg.dbg, config=cfg, space=space,
+        meta={"fetch_mode": fetch_mode, "K": t.K, "nsub": t.nsub, "n": t.n,
+              "smem_tables": [x[0] for x in smem], "lut_entries": len(lut)})

@@ -1,0 +1,152 @@
+"""CUDA path vs the oracle / the reference's golden vectors (needs a B200).
+
+Bar (north_star): lattice shift k and sub-region index bit-exact for every
+query and coset; values within 1e-5 relative (f32 kernels vs the fp64
+reference) and 1e-12 for the f64 variant.  Every test goes through the C ABI
+(libsplinegpu.so) with an NVRTC-compiled sm_100a kernel.
+"""
+
+import itertools
+
+import numpy as np
+import pytest
+
+from oracle import refeval
+from tests.gpu_util import (ATOL_F32, ATOL_F64, RTOL_F32, RTOL_F64, close, golden_names,
+                            load_golden)
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+SETS = ("uniform", "grid", "adversarial")
+
+
+def _evaluator(space, arrays, **kw):
+    from paper_2102_08518_b200 import Evaluator, GenConfig, ScheduleParams
+    n = space.stencil_size
+    params = kw.pop("params", ScheduleParams(1, n, "predicated"))
+    fw = kw.pop("float_width", "f32")
+    dt = np.float32 if fw == "f32" else np.float64
+    cfg = GenConfig(params=params, float_width=fw, **kw)
+    return Evaluator(space, [a.astype(dt) for a in arrays], cfg)
+
+
+def _xs(z, which, dtype=torch.float32):
+    return torch.from_numpy(z[f"{which}_xs"].astype(np.float64)).to(dtype).cuda()
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_selection_bit_exact(name):
+    space, _, z, arrays = load_golden(name)
+    ev = _evaluator(space, arrays, dbg=True)
+    for which in SETS:
+        out, _, dbg = ev(_xs(z, which))
+        dbg = dbg.cpu().numpy()
+        k_want, sub_want = z[f"{which}_k"], z[f"{which}_sub"]
+        s = space.dim
+        for ci in range(space.ncosets):
+            assert np.array_equal(dbg[:, ci, :s], k_want[ci]), (which, ci)
+            assert np.array_equal(dbg[:, ci, s], sub_want[ci]), (which, ci)
+
+
+CONFIGS = [
+    dict(),
+    dict(form="sites"),
+    dict(coeffs="lut"),
+    dict(unroll_cosets=False),
+    dict(params_mode="branchy"),
+    dict(params_mode="branchy", form="sites"),
+    dict(params_md=(2, 4)),
+    dict(params_md=(2, 4), refetch=True),
+    dict(block=256),
+]
+
+
+def _cfg(space, spec):
+    from paper_2102_08518_b200 import ScheduleParams
+    spec = dict(spec)
+    n = space.stencil_size
+    m, d = spec.pop("params_md", (1, n))
+    m, d = min(m, n), min(max(d, min(m, n)), n)
+    mode = spec.pop("params_mode", "predicated")
+    refetch = spec.pop("refetch", False)
+    spec["params"] = ScheduleParams(m, d, mode, refetch)
+    return spec
+
+
+@pytest.mark.parametrize("name", golden_names())
+@pytest.mark.parametrize("ci", range(len(CONFIGS)))
+def test_values_f32_vs_reference(name, ci):
+    space, _, z, arrays = load_golden(name)
+    ev = _evaluator(space, arrays, **_cfg(space, CONFIGS[ci]))
+    for which in SETS:
+        got = ev(_xs(z, which)).double().cpu().numpy()
+        want = z[f"{which}_value"]
+        ok = close(got, want, RTOL_F32, ATOL_F32)
+        assert ok.all(), (which, float(np.abs(got - want).max()))
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_values_f64_variant(name):
+    space, _, z, arrays = load_golden(name)
+    for spec in (dict(), dict(params_mode="branchy", form="sites"), dict(unroll_cosets=False)):
+        ev = _evaluator(space, arrays, float_width="f64", **_cfg(space, spec))
+        for which in SETS:
+            got = ev(_xs(z, which, torch.float64)).cpu().numpy()
+            want = z[f"{which}_value"]
+            ok = close(got, want, RTOL_F64, ATOL_F64)
+            assert ok.all(), (which, spec, float(np.abs(got - want).max()))
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_gradient_vs_oracle(name):
+    space, ospace, z, arrays = load_golden(name)
+    xs = z["uniform_xs"].astype(np.float64)
+    _, gwant = refeval.reference_eval_batch(ospace, xs, [a.astype(np.float64) for a in arrays],
+                                            grad=True)
+    ev = _evaluator(space, arrays, grad=True)
+    out, g, _ = ev(_xs(z, "uniform"))
+    g = g.double().cpu().numpy()
+    scale = max(1.0, float(np.abs(gwant).max()))
+    assert np.abs(g - gwant).max() <= 1e-5 * scale
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_host_path_matches_device_path(name):
+    space, _, z, arrays = load_golden(name)
+    ev = _evaluator(space, arrays)
+    xs = z["uniform_xs"]
+    dev = ev(torch.from_numpy(xs).cuda()).cpu().numpy()
+    host = ev.eval_host(xs, chunk=257)
+    assert np.array_equal(dev, host)
+
+
+def test_unreachable_sigma_raises():
+    """sigma == -1 -> UnreachableRegionError (reference ir.py:757-766, oracle.py:69-73)."""
+    import dataclasses
+    from paper_2102_08518_b200 import Evaluator, GenConfig, ScheduleParams, UnreachableRegionError
+    from paper_2102_08518_b200.cudagen import generate
+    from paper_2102_08518_b200.model import SubRegionIndexer
+    space, _, z, arrays = load_golden("zp")
+    sig = list(space.indexer.sigma)
+    sig[0] = -1   # q == 0: x0 - x1 < 0 and x0 + x1 < 0
+    bad = dataclasses.replace(space, indexer=SubRegionIndexer(4, tuple(sig)))
+    prog = generate(bad, GenConfig(ScheduleParams(1, 7)), (8, 8), validate=False)
+    ev = Evaluator(bad, arrays, prog=prog)
+    ev(torch.tensor([[0.1, 0.3]], dtype=torch.float32).cuda())          # q = 2: fine
+    with pytest.raises(UnreachableRegionError):
+        ev(torch.tensor([[-0.3, 0.1]], dtype=torch.float32).cuda())     # q = 0
+    ev(torch.tensor([[0.1, 0.3]], dtype=torch.float32).cuda())          # flag was cleared
+
+
+def test_reference_contract_interpret_batch():
+    """interpret_batch keeps the reference signature: numpy in, numpy (N,) out."""
+    from paper_2102_08518_b200 import DataVolume, GenConfig, ScheduleParams, generate, interpret_batch
+    space, _, z, arrays = load_golden("trilinear_voronoi")
+    data = DataVolume(arrays)
+    prog = generate(space, GenConfig(ScheduleParams(2, 5, "branchy")), (6, 6, 6))
+    xs = z["uniform_xs"].astype(np.float64)
+    got = interpret_batch(prog, xs, data)
+    assert got.shape == (xs.shape[0],) and got.dtype == np.float64
+    assert close(got, z["uniform_value"], RTOL_F32, ATOL_F32).all()
