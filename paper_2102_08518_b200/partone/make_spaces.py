@@ -47,5 +47,44 @@ def main(argv):
     return 0
 
 
+# -- box / Voronoi spline spaces built by the Part-I producer ---------------------------
+
+from fractions import Fraction as _F  # noqa: E402
+
+_H = _F(1, 2)
+BCC_COSETS = [(0, 0, 0), (_H, _H, _H)]
+BCC_GEN = [[1, 0, _H], [0, 1, _H], [0, 0, _H]]
+BCC_DIRS = [(_H, _H, _H), (_H, -_H, -_H), (-_H, _H, -_H), (-_H, -_H, _H)]
+FCC_COSETS = [(0, 0, 0), (_H, _H, 0), (_H, 0, _H), (0, _H, _H)]
+FCC_GEN = [[_H, _H, 0], [_H, 0, _H], [0, _H, _H]]
+FCC_DIRS = [(_H, _H, 0), (_H, -_H, 0), (_H, 0, _H), (_H, 0, -_H), (0, _H, _H), (0, _H, -_H)]
+
+
+def _produce(phi, cosets, gen, name, rounding="round_nearest"):
+    from .producer import Producer
+    return Producer(phi, cosets, gen, name, rounding).run()
+
+
+@register("bcc_box5", (8, 8, 8))
+def _bcc_box5():
+    """C2: BCC quintic box spline -- the 4 BCC nearest-neighbour directions, each twice."""
+    from .boxspline import centered_box
+    return _produce(centered_box(BCC_DIRS, [2, 2, 2, 2]), BCC_COSETS, BCC_GEN, "bcc_box5")
+
+
+@register("bcc_box_linear", (8, 8, 8))
+def _bcc_box_linear():
+    """The BCC linear (rhombic-dodecahedron) box spline: the 4 directions once."""
+    from .boxspline import centered_box
+    return _produce(centered_box(BCC_DIRS), BCC_COSETS, BCC_GEN, "bcc_box_linear")
+
+
+@register("fcc_box6", (6, 6, 6))
+def _fcc_box6():
+    """C4: FCC 6-direction (cubic truncated-octahedron) box spline."""
+    from .boxspline import centered_box
+    return _produce(centered_box(FCC_DIRS), FCC_COSETS, FCC_GEN, "fcc_box6")
+
+
 if __name__ == "__main__":
     raise SystemExit(main(sys.argv[1:]))
