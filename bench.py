@@ -159,13 +159,17 @@ class ClockSampler:
 # -- CPU baseline (oracle port; test-infrastructure import, baseline leg only) ---------------
 
 
-def _cpu_worker(args):
-    space_path, arrays, xs = args
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
+_CPU_STATE = {}
+
+
+def _cpu_worker(i):
+    """Evaluate shard i of the sample (state inherited copy-on-write through fork)."""
     from oracle import refeval
-    sp = refeval.load_space_file(space_path)
+    st = _CPU_STATE
+    sp = refeval.load_space_file(st["path"])
+    xs = st["xs"][i * st["shard"]:(i + 1) * st["shard"]].astype(np.float64)
     t0 = time.perf_counter()
-    refeval.reference_eval_batch(sp, xs, arrays)
+    refeval.reference_eval_batch(sp, xs, st["arrays"])
     return time.perf_counter() - t0
 
 
@@ -175,19 +179,19 @@ def cpu_baseline(space_name, arrays_f32, xs_f32, budget_s=15.0, shard=1 << 14):
     import multiprocessing as mp
     from paper_2102_08518_b200.model import SPACES_DIR
     path = str(SPACES_DIR / f"{space_name}.json")
-    arrays = [a.astype(np.float64) for a in arrays_f32]
+    for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[k] = "1"
+    _CPU_STATE.update(path=path, arrays=[a.astype(np.float64) for a in arrays_f32],
+                      xs=xs_f32, shard=shard)
     cores = len(os.sched_getaffinity(0))
-    # calibrate on one shard
-    t1 = _cpu_worker((path, arrays, xs_f32[:shard].astype(np.float64)))
+    t1 = _cpu_worker(0)     # calibrate on one shard
     rate1 = shard / t1
     nshards = max(cores, int(budget_s * rate1 * cores / shard) // cores * cores)
     nshards = min(nshards, max(1, len(xs_f32) // shard))
-    jobs = [(path, arrays, xs_f32[i * shard:(i + 1) * shard].astype(np.float64))
-            for i in range(nshards)]
     ctx = mp.get_context("fork")
     t0 = time.perf_counter()
     with ctx.Pool(cores) as pool:
-        pool.map(_cpu_worker, jobs)
+        pool.map(_cpu_worker, range(nshards))
     wall = time.perf_counter() - t0
     n = nshards * shard
     return {"value": n / wall / 1e9, "unit": "Grecon/s", "cores": cores, "kind": "port",
