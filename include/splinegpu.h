@@ -66,10 +66,24 @@ typedef struct sg_module_info {
   int32_t block;               /* threads per CTA */
   int32_t has_grad;            /* kernel writes grad (N, s) */
   int32_t has_dbg;             /* kernel writes dbg (N, M, s+1): k then sub-region */
-  int32_t halo;                /* ghost-halo width the kernel's fetch offsets assume */
+  int32_t halo;                /* padded index of interior element 0 on every axis */
   int32_t queries_per_thread;  /* >= 1 */
-  int64_t padded_extents[SG_MAX_COSETS][SG_MAX_DIM]; /* per coset, E + 2*halo */
+  int64_t padded_extents[SG_MAX_COSETS][SG_MAX_DIM]; /* per coset allocation extents */
+  /* binned mode (SG_MODE_BINNED): queries are counting-sorted into bins of
+   * `bin` lattice cells of coset 0; one CTA per bin stages the bin's coefficient
+   * bricks (all cosets) in shared memory -- by TMA when stage_tma -- and gathers
+   * from there.  Direct mode gathers through L1/L2. */
+  int32_t mode;                /* SG_MODE_DIRECT | SG_MODE_BINNED */
+  int32_t rounding;            /* coset-0 region map: SG_FLOOR | SG_ROUND */
+  int32_t stage_tma;           /* 1: bricks staged with cp.async.bulk.tensor */
+  int32_t smem_bytes;          /* dynamic shared memory of the binned kernel */
+  int32_t bin;                 /* bin edge, in lattice cells */
+  int32_t brick[SG_MAX_DIM];   /* brick extent per axis (elements), C order */
+  int64_t extents[SG_MAX_DIM]; /* unpadded extents (equal for all cosets in binned mode) */
 } sg_module_info;
+
+enum { SG_MODE_DIRECT = 0, SG_MODE_BINNED = 1 };
+enum { SG_FLOOR = 0, SG_ROUND = 1 };
 
 int sg_version(void);
 const char* sg_last_error(void);
@@ -91,10 +105,13 @@ int sg_module_regs(const sg_module* m, int* regs_per_thread, int* local_bytes);
 int sg_module_status(sg_module* m, void* stream, uint32_t* flags);
 
 /* extents: ncosets x dim (row-major); src[c] points to coset c's C-order array of
- * prod(extents[c]) elements, in HOST memory (src_on_device == 0) or device memory. */
+ * prod(extents[c]) elements, in HOST memory (src_on_device == 0) or device memory.
+ * The device copy is periodic: padded element i holds src[(i - halo) mod E] on every
+ * axis; padded (ncosets x dim, may be NULL = E + 2*halo) gives the allocation extents
+ * a module asks for (sg_module_info.padded_extents). */
 int sg_volume_create(int device, int dim, int ncosets, const int64_t* extents, int halo,
-                     int dtype, const void* const* src, int src_on_device, void* stream,
-                     sg_volume** out);
+                     const int64_t* padded, int dtype, const void* const* src,
+                     int src_on_device, void* stream, sg_volume** out);
 int sg_volume_free(sg_volume* v);
 int sg_volume_bytes(const sg_volume* v, int64_t* bytes);
 /* Device address of coset c's padded array origin (for tests / peer copies). */

@@ -109,7 +109,8 @@ class Evaluator:
             raise InterpreterError(f"program compiled for extents {self.prog.extents}, data has {ext}")
         self.device = device
         self.module = runtime.Module(self.prog, device)
-        self.volume = runtime.Volume(arrays, self.prog.halo, self.prog.dtype, device)
+        self.volume = runtime.Volume(arrays, self.prog.halo, self.prog.dtype, device,
+                                     padded=self.prog.padded_extents)
         self.torch_dtype = torch.float32 if self.prog.float_width == "f32" else torch.float64
 
     def __call__(self, xs, out=None, grad=None, dbg=None, check=True):

@@ -6,6 +6,7 @@
 // dynamically from the image's CUDA 12.9 toolkit.  Generated kernels are loaded
 // with the context-independent library API (cudaLibraryLoadData) and launched
 // with cudaLaunchKernel, so no driver-API symbols are needed.
+#include <cuda.h>  // CUtensorMap & friends (types only; the encoder is fetched at run time)
 #include <cuda_runtime.h>
 #include <nvrtc.h>
 
@@ -50,6 +51,29 @@ struct SgCosets {  // must match the struct emitted by cudagen.py
   const void* base[SG_MAX_COSETS];
 };
 
+struct SgTmaps {  // must match cudagen.py: one TMA descriptor per coset
+  CUtensorMap m[SG_MAX_COSETS];
+};
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  });
+  return fn;
+}
+
 }  // namespace
 
 struct sg_module {
@@ -63,6 +87,12 @@ struct sg_module {
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
   cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
+  // binned mode: sorted queries + per-bin counts/starts/cursors (one stream at a time)
+  std::mutex bin_mu;
+  void* bin_scratch = nullptr;
+  size_t bin_scratch_bytes = 0;
+  int64_t nbins = 0;
+  int64_t nb[SG_MAX_DIM] = {1, 1, 1, 1};
 };
 
 struct sg_volume {
@@ -100,6 +130,120 @@ __global__ void sg_pad_kernel(T* __restrict__ dst, const T* __restrict__ src, in
       mul *= ee[d];
     }
     dst[i] = src[src_idx];
+  }
+}
+
+
+// ---- binned mode: counting sort of the queries by coset-0 lattice cell ------------------
+//
+// The bin of a query is computed from k0 = rho(x) of coset 0 (offset 0, identity basis),
+// with exactly the fp64 operations the generated kernel uses, so both agree on k0.
+struct BinGeom {
+  int dim, rounding, bin;
+  long long ext[3];
+  long long nb[3];
+  long long nbins;
+};
+
+__device__ __forceinline__ long long sg_rho0(double x, int rounding) {
+  if (rounding == SG_ROUND)
+    return (long long)(x >= 0.0 ? floor(__dadd_rn(x, 0.5)) : ceil(__dsub_rn(x, 0.5)));
+  return (long long)floor(x);
+}
+
+__device__ __forceinline__ int sg_bin_of(const float* __restrict__ xs, long long i,
+                                         const BinGeom& g) {
+  long long lin = 0;
+  for (int d = 0; d < g.dim; ++d) {
+    long long k = sg_rho0((double)xs[i * g.dim + d], g.rounding);
+    long long kw = k % g.ext[d];
+    if (kw < 0) kw += g.ext[d];
+    lin = lin * g.nb[d] + kw / g.bin;
+  }
+  return (int)lin;
+}
+
+constexpr int SG_BIN_CHUNK = 4096;      // queries per histogram / scatter CTA
+constexpr int SG_SMEM_BINS = 12288;     // bins that fit a privatized shared histogram
+
+__global__ void sg_bin_count(const float* __restrict__ xs, long long n, BinGeom g,
+                             int* __restrict__ counts) {
+  extern __shared__ int hist[];
+  const bool priv = g.nbins <= SG_SMEM_BINS;
+  if (priv)
+    for (int b = threadIdx.x; b < g.nbins; b += blockDim.x) hist[b] = 0;
+  __syncthreads();
+  const long long lo = (long long)blockIdx.x * SG_BIN_CHUNK;
+  const long long hi = min(n, lo + SG_BIN_CHUNK);
+  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    int b = sg_bin_of(xs, i, g);
+    if (priv)
+      atomicAdd(&hist[b], 1);
+    else
+      atomicAdd(&counts[b], 1);
+  }
+  __syncthreads();
+  if (priv)
+    for (int b = threadIdx.x; b < g.nbins; b += blockDim.x)
+      if (hist[b]) atomicAdd(&counts[b], hist[b]);
+}
+
+// exclusive scan of counts -> starts[0..nbins], cursors = starts (one CTA of 1024)
+__global__ void sg_bin_scan(const int* __restrict__ counts, long long nbins,
+                            int* __restrict__ starts, int* __restrict__ cursors) {
+  __shared__ int part[1024];
+  const int t = threadIdx.x;
+  const long long per = (nbins + 1023) / 1024;
+  const long long lo = t * per, hi = min(nbins, lo + per);
+  int sum = 0;
+  for (long long b = lo; b < hi; ++b) sum += counts[b];
+  part[t] = sum;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    int v = t >= off ? part[t - off] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  int run = part[t] - sum;  // exclusive prefix of this thread's slice
+  for (long long b = lo; b < hi; ++b) {
+    starts[b] = run;
+    cursors[b] = run;
+    run += counts[b];
+  }
+  if (t == 1023) starts[nbins] = part[1023];
+}
+
+__global__ void sg_bin_scatter(const float* __restrict__ xs, long long n, BinGeom g,
+                               int* __restrict__ cursors, float4* __restrict__ sorted) {
+  extern __shared__ int sh[];
+  int* hist = sh;                 // per-CTA counts, then running local offsets
+  int* base = sh + SG_SMEM_BINS;  // reserved global position per bin
+  const bool priv = g.nbins <= SG_SMEM_BINS;
+  const long long lo = (long long)blockIdx.x * SG_BIN_CHUNK;
+  const long long hi = min(n, lo + SG_BIN_CHUNK);
+  if (priv) {
+    for (int b = threadIdx.x; b < g.nbins; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x)
+      atomicAdd(&hist[sg_bin_of(xs, i, g)], 1);
+    __syncthreads();
+    for (int b = threadIdx.x; b < g.nbins; b += blockDim.x) {
+      int c = hist[b];
+      base[b] = c ? atomicAdd(&cursors[b], c) : 0;
+      hist[b] = 0;
+    }
+    __syncthreads();
+  }
+  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    int b = sg_bin_of(xs, i, g);
+    int pos = priv ? base[b] + atomicAdd(&hist[b], 1) : atomicAdd(&cursors[b], 1);
+    float4 r;
+    r.x = xs[i * g.dim];
+    r.y = g.dim > 1 ? xs[i * g.dim + 1] : 0.f;
+    r.z = g.dim > 2 ? xs[i * g.dim + 2] : 0.f;
+    r.w = __int_as_float((int)i);
+    sorted[pos] = r;
   }
 }
 
@@ -201,6 +345,32 @@ int sg_module_load(const void* image, size_t image_len, const char* entry, int d
   } else {
     cudaGetLastError();
   }
+  if (m->info.mode == SG_MODE_BINNED) {
+    if (m->info.dtype != SG_F32 || m->info.dim > 3) {
+      cudaLibraryUnload(m->lib);
+      delete m;
+      return fail(SG_EINVAL, "binned mode supports f32 volumes of dimension <= 3");
+    }
+    m->nbins = 1;
+    for (int d = 0; d < m->info.dim; ++d) {
+      m->nb[d] = (m->info.extents[d] + m->info.bin - 1) / m->info.bin;
+      m->nbins *= m->nb[d];
+    }
+    if (m->nbins > (1LL << 30)) {
+      cudaLibraryUnload(m->lib);
+      delete m;
+      return fail(SG_EINVAL, "too many bins");
+    }
+    if (m->info.smem_bytes > 48 * 1024) {
+      e = cudaFuncSetAttribute((const void*)m->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               m->info.smem_bytes);
+      if (e != cudaSuccess) {
+        cudaLibraryUnload(m->lib);
+        delete m;
+        return fail(SG_ECUDA, "smem attribute: %s", cudaGetErrorString(e));
+      }
+    }
+  }
   e = cudaMalloc(&m->d_err, sizeof(unsigned));
   if (e == cudaSuccess) e = cudaMemset(m->d_err, 0, sizeof(unsigned));
   if (e != cudaSuccess) {
@@ -218,6 +388,7 @@ int sg_module_free(sg_module* m) {
   for (auto& s : m->streams)
     if (s) cudaStreamDestroy(s);
   if (m->scratch) cudaFree(m->scratch);
+  if (m->bin_scratch) cudaFree(m->bin_scratch);
   if (m->d_err) cudaFree(m->d_err);
   if (m->lib) cudaLibraryUnload(m->lib);
   delete m;
@@ -245,8 +416,8 @@ int sg_module_status(sg_module* m, void* stream, uint32_t* flags) {
 }
 
 int sg_volume_create(int device, int dim, int ncosets, const int64_t* extents, int halo,
-                     int dtype, const void* const* src, int src_on_device, void* stream,
-                     sg_volume** out) {
+                     const int64_t* padded, int dtype, const void* const* src,
+                     int src_on_device, void* stream, sg_volume** out) {
   if (!extents || !src || !out) return fail(SG_EINVAL, "NULL argument");
   if (dim < 1 || dim > SG_MAX_DIM) return fail(SG_EINVAL, "bad dim %d", dim);
   if (ncosets < 1 || ncosets > SG_MAX_COSETS) return fail(SG_EINVAL, "bad coset count %d", ncosets);
@@ -271,7 +442,12 @@ int sg_volume_create(int device, int dim, int ncosets, const int64_t* extents, i
         return fail(SG_EINVAL, "extents must be positive");
       }
       v->ext[c][d] = e;
-      v->pext[c][d] = e + 2 * halo;
+      v->pext[c][d] = padded ? padded[c * dim + d] : e + 2 * halo;
+      if (v->pext[c][d] < e + halo) {
+        delete v;
+        return fail(SG_EINVAL, "padded extent %lld too small for extent %lld + halo %d",
+                    (long long)v->pext[c][d], (long long)e, halo);
+      }
       n *= v->pext[c][d];
     }
     off = (off + 255) & ~size_t(255);
@@ -391,6 +567,8 @@ static int check_pair(const sg_module* m, const sg_volume* v) {
     return fail(SG_EINVAL, "data has %d cosets, program wants %d", v->ncosets, in.ncosets);
   if (v->dtype != in.dtype) return fail(SG_EINVAL, "volume dtype does not match the kernel");
   if (v->device != m->device) return fail(SG_EINVAL, "volume and module on different devices");
+  if (v->halo != in.halo)
+    return fail(SG_EINVAL, "volume halo %d, kernel compiled for %d", v->halo, in.halo);
   for (int c = 0; c < in.ncosets; ++c)
     for (int d = 0; d < in.dim; ++d)
       if (v->pext[c][d] != in.padded_extents[c][d])
@@ -401,9 +579,93 @@ static int check_pair(const sg_module* m, const sg_volume* v) {
   return SG_OK;
 }
 
+static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64_t n, void* out,
+                         void* grad, int32_t* dbg, cudaStream_t st) {
+  const sg_module_info& in = m->info;
+  std::lock_guard<std::mutex> lock(m->bin_mu);
+  const size_t nb = (size_t)m->nbins;
+  const size_t need = (size_t)n * sizeof(float4) + (3 * nb + 1) * sizeof(int) + 256;
+  if (m->bin_scratch_bytes < need) {
+    if (m->bin_scratch) cudaFree(m->bin_scratch);
+    m->bin_scratch = nullptr;
+    m->bin_scratch_bytes = 0;
+    CU(cudaMalloc(&m->bin_scratch, need));
+    m->bin_scratch_bytes = need;
+  }
+  float4* sorted = (float4*)m->bin_scratch;
+  int* counts = (int*)(sorted + n);
+  int* starts = counts + nb;
+  int* cursors = starts + nb + 1;
+  BinGeom g{};
+  g.dim = in.dim;
+  g.rounding = in.rounding;
+  g.bin = in.bin;
+  for (int d = 0; d < 3; ++d) {
+    g.ext[d] = d < in.dim ? in.extents[d] : 1;
+    g.nb[d] = d < in.dim ? m->nb[d] : 1;
+  }
+  g.nbins = (long long)nb;
+  CU(cudaMemsetAsync(counts, 0, nb * sizeof(int), st));
+  const long long chunks = (n + SG_BIN_CHUNK - 1) / SG_BIN_CHUNK;
+  const bool priv = nb <= (size_t)SG_SMEM_BINS;
+  size_t sh1 = priv ? nb * sizeof(int) : 0;
+  size_t sh3 = priv ? 2 * SG_SMEM_BINS * sizeof(int) : 0;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(sg_bin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         2 * SG_SMEM_BINS * sizeof(int));
+    cudaFuncSetAttribute(sg_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         SG_SMEM_BINS * sizeof(int));
+    attr_set = true;
+  }
+  sg_bin_count<<<(unsigned)chunks, 512, sh1, st>>>((const float*)xs, (long long)n, g, counts);
+  CU(cudaGetLastError());
+  sg_bin_scan<<<1, 1024, 0, st>>>(counts, (long long)nb, starts, cursors);
+  CU(cudaGetLastError());
+  sg_bin_scatter<<<(unsigned)chunks, 512, sh3, st>>>((const float*)xs, (long long)n, g, cursors,
+                                                     sorted);
+  CU(cudaGetLastError());
+  SgCosets cs{};
+  for (int c = 0; c < v->ncosets; ++c) cs.base[c] = v->origin[c];
+  static thread_local SgTmaps tm;
+  memset(&tm, 0, sizeof tm);
+  if (in.stage_tma) {
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc) return fail(SG_ECUDA, "cuTensorMapEncodeTiled is unavailable");
+    for (int c = 0; c < v->ncosets; ++c) {
+      cuuint64_t gdim[SG_MAX_DIM], gstr[SG_MAX_DIM];
+      cuuint32_t box[SG_MAX_DIM], estr[SG_MAX_DIM];
+      const int s = in.dim;
+      long long stride = sizeof(float);
+      for (int d = 0; d < s; ++d) {  // TMA dims are innermost-first
+        const int ax = s - 1 - d;
+        gdim[d] = (cuuint64_t)v->pext[c][ax];
+        box[d] = (cuuint32_t)in.brick[ax];
+        estr[d] = 1;
+        if (d > 0) gstr[d - 1] = (cuuint64_t)stride;
+        stride *= v->pext[c][ax];
+      }
+      void* gaddr = (char*)v->alloc + v->coset_off[c];
+      CUresult r = enc(&tm.m[c], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)s, gaddr, gdim,
+                       gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return fail(SG_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    }
+  }
+  unsigned* err = m->d_err;
+  const void* sp = sorted;
+  const void* stp = starts;
+  void* args[] = {(void*)&sp, (void*)&stp, (void*)&out, (void*)&grad, (void*)&dbg, (void*)&err,
+                  (void*)&cs, (void*)&tm};
+  CU(cudaLaunchKernel((const void*)m->kernel, dim3((unsigned)nb), dim3(in.block), args,
+                      (size_t)in.smem_bytes, st));
+  return SG_OK;
+}
+
 static int launch(sg_module* m, const sg_volume* v, const void* xs, int64_t n, void* out,
                   void* grad, int32_t* dbg, cudaStream_t st) {
   if (n <= 0) return SG_OK;
+  if (m->info.mode == SG_MODE_BINNED) return launch_binned(m, v, xs, n, out, grad, dbg, st);
   SgCosets cs{};
   for (int c = 0; c < v->ncosets; ++c) cs.base[c] = v->origin[c];
   long long nn = (long long)n;

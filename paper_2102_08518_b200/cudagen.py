@@ -59,6 +59,9 @@ class GenConfig:
     grad: bool = False
     dbg: bool = False
     min_blocks: int = 0          # __launch_bounds__ second argument (0 = let ptxas pick)
+    mode: str = "direct"         # "direct": gathers through L1/L2; "binned": bin + smem bricks
+    bin: int = 8                 # binned: bin edge in lattice cells
+    stage: str = "tma"           # binned: brick staging, "tma" (cp.async.bulk.tensor) | "ldg"
 
     def __post_init__(self):
         if self.float_width not in (F64, F32):
@@ -69,6 +72,10 @@ class GenConfig:
             raise ValueError(f"coeffs must be one of {COEFFS}")
         if self.block % 32 or not 32 <= self.block <= 1024:
             raise ValueError("block must be a multiple of 32 in [32, 1024]")
+        if self.mode not in ("direct", "binned"):
+            raise ValueError("mode must be 'direct' or 'binned'")
+        if self.stage not in ("tma", "ldg"):
+            raise ValueError("stage must be 'tma' or 'ldg'")
 
 
 def default_config(space: SplineSpace, **kw) -> GenConfig:
@@ -281,6 +288,12 @@ class CudaProgram:
     has_dbg: bool
     config: GenConfig
     space: SplineSpace = field(repr=False)
+    mode: str = "direct"
+    bin: int = 0
+    brick: tuple = ()
+    smem_bytes: int = 0
+    stage_tma: bool = False
+    rounding: int = 1
     meta: dict = field(default_factory=dict)
 
     @property
@@ -357,7 +370,34 @@ def generate(space, config: GenConfig | None = None, extents=None,
     if len(ext) != M or any(len(e) != s for e in ext):
         raise ValueError(f"extents must give {s} values for each of {M} cosets")
     h = t.halo
-    pext = tuple(tuple(e + 2 * h for e in row) for row in ext)
+    binned = cfg.mode == "binned"
+    bin_ = cfg.bin
+    rm0 = space.region_map
+    if binned:
+        if cfg.float_width != F32 or s > 3:
+            raise ValueError("binned mode supports f32 kernels of dimension <= 3")
+        if rm0.shape == PARALLELEPIPED and not exact.is_identity(rm0.basis):
+            raise ValueError("binned mode needs an identity region-of-evaluation basis")
+        if len(set(ext)) != 1:
+            raise ValueError("binned mode needs equal coset extents")
+        if any(not (0 <= c < 1) for off in t.cosets for c in off):
+            raise ValueError("binned mode needs coset offsets in [0, 1)")
+        H = h + 1
+        unit = 4  # TMA: innermost box extent x 4 B must be a multiple of 16 B
+        brick = [bin_ + 2 * h + 2] * s
+        brick[-1] = -(-brick[-1] // unit) * unit
+        nb = [-(-e // bin_) for e in ext[0]]
+        prow = [max(ext[0][d] + 2 * H, (nb[d] - 1) * bin_ + brick[d]) for d in range(s)]
+        prow[-1] = -(-prow[-1] // unit) * unit
+        pext = tuple(tuple(prow) for _ in range(M))
+        bstr = [1] * s
+        for d in range(s - 2, -1, -1):
+            bstr[d] = bstr[d + 1] * brick[d + 1]
+        brick_elems = bstr[0] * brick[0]
+        smem_bytes = 128 * (-(-(M * brick_elems * 4) // 128))
+    else:
+        H = h
+        pext = tuple(tuple(e + 2 * h for e in row) for row in ext)
     for row in pext:
         nel = 1
         for e in row:
@@ -371,6 +411,9 @@ def generate(space, config: GenConfig | None = None, extents=None,
             st[d] = st[d + 1] * row[d + 1]
         strides.append(st)
     same_geom = len(set(pext)) == 1
+    if binned:
+        strides = [list(bstr) for _ in range(M)]   # fetch offsets are brick-relative
+        same_geom = True
 
     fw = cfg.float_width
     em = Emitter(fw)
@@ -392,8 +435,12 @@ def generate(space, config: GenConfig | None = None, extents=None,
       f"refetch={str(refetch).lower()} unroll_cosets={str(cfg.unroll_cosets).lower()} "
       f"form={cfg.form} coeffs={cfg.coeffs} {fw} block={cfg.block} grad={int(cfg.grad)} "
       f"dbg={int(cfg.dbg)}")
-    A(f"// extents={ext} halo={h}")
+    A(f"// extents={ext} stencil reach={h} padded={pext[0]} halo={H} mode={cfg.mode}"
+      + (f" bin={bin_} brick={tuple(brick)} stage={cfg.stage}" if binned else ""))
     A("struct SgCosets { const void* base[8]; };")
+    if binned:
+        A("struct __align__(64) SgTmap { unsigned long long opaque[16]; };")
+        A("struct SgTmaps { SgTmap m[8]; };")
 
     # ---- tables ------------------------------------------------------------
     smem = []     # (name, ctype, values)
@@ -452,33 +499,112 @@ def generate(space, config: GenConfig | None = None, extents=None,
     lb = f"{cfg.block}, {cfg.min_blocks}" if cfg.min_blocks else f"{cfg.block}"
     body = []
     B = body.append
-    B(f'extern "C" __global__ void __launch_bounds__({lb}) {ENTRY}(')
-    B(f"    const {T}* __restrict__ xs, long long n, {T}* __restrict__ out, {T}* __restrict__ grad,")
-    B("    int* __restrict__ dbg, unsigned* __restrict__ err, SgCosets vol) {")
-    for name, ctype, vals in smem:
-        B(f"  __shared__ {ctype} {name}[{len(vals)}];")
-    for name, ctype, vals in smem:
-        B(f"  for (int i_ = threadIdx.x; i_ < {len(vals)}; i_ += {cfg.block}) {name}[i_] = {name}_c[i_];")
-    if smem:
+    if not binned:
+        B(f'extern "C" __global__ void __launch_bounds__({lb}) {ENTRY}(')
+        B(f"    const {T}* __restrict__ xs, long long n, {T}* __restrict__ out, {T}* __restrict__ grad,")
+        B("    int* __restrict__ dbg, unsigned* __restrict__ err, SgCosets vol) {")
+        for name, ctype, vals in smem:
+            B(f"  __shared__ {ctype} {name}[{len(vals)}];")
+        for name, ctype, vals in smem:
+            B(f"  for (int i_ = threadIdx.x; i_ < {len(vals)}; i_ += {cfg.block}) {name}[i_] = {name}_c[i_];")
+        if smem:
+            B("  __syncthreads();")
+        B(f"  const long long qi = (long long)blockIdx.x * {cfg.block} + threadIdx.x;")
+        B("  if (qi >= n) return;")
+        for d in range(s):
+            B(f"  const double x{d} = (double)xs[qi * {s} + {d}];")
+        ind = "  "
+    else:
+        B(f'extern "C" __global__ void __launch_bounds__({lb}) {ENTRY}(')
+        B("    const float4* __restrict__ sorted, const int* __restrict__ starts,")
+        B(f"    {T}* __restrict__ out, {T}* __restrict__ grad, int* __restrict__ dbg,")
+        B("    unsigned* __restrict__ err, SgCosets vol, const __grid_constant__ SgTmaps tm) {")
+        B("  extern __shared__ __align__(128) float sg_brick[];")
+        B("  __shared__ __align__(8) unsigned long long sg_bar;")
+        for name, ctype, vals in smem:
+            B(f"  __shared__ {ctype} {name}[{len(vals)}];")
+        # bin coordinates (row-major over nb)
+        B("  const int bin = blockIdx.x;")
+        rem = "bin"
+        for d in range(s - 1, -1, -1):
+            if d == 0:
+                B(f"  const int lo0 = ({rem}) * {bin_};")
+            else:
+                B(f"  const int lo{d} = (({rem}) % {nb[d]}) * {bin_};")
+                rem = f"({rem}) / {nb[d]}"
+        gst = [1] * s
+        for d in range(s - 2, -1, -1):
+            gst[d] = gst[d + 1] * pext[0][d + 1]
+        if cfg.stage == "tma":
+            coords = ", ".join(f"%{2 + i}" for i in range(s))
+            cvals = ", ".join(f'"r"(lo{d})' for d in range(s - 1, -1, -1))
+            B("  const unsigned sg_bar_a = (unsigned)__cvta_generic_to_shared(&sg_bar);")
+            B("  if (threadIdx.x == 0) {")
+            B('    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(sg_bar_a) : "memory");')
+            B('    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");')
+            B('    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");')
+            B(f'    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(sg_bar_a), "r"({M * brick_elems * 4}) : "memory");')
+            for l in range(M):
+                B(f"    {{ const unsigned dst = (unsigned)__cvta_generic_to_shared(sg_brick + {l * brick_elems});")
+                B(f'      asm volatile("cp.async.bulk.tensor.{s}d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {{{coords}}}], [%{2 + s}];"')
+                B(f'                   :: "r"(dst), "l"((unsigned long long)&tm.m[{l}]), {cvals}, "r"(sg_bar_a) : "memory"); }}')
+            B("  }")
+        else:
+            bz = brick[-1]
+            for l in range(M):
+                off0 = sum(H * gst[d] for d in range(s))
+                B(f"  {{ const float* __restrict__ G = (const float*)vol.base[{l}] - {off0};")
+                B(f"    for (int e_ = threadIdx.x; e_ < {brick_elems}; e_ += {cfg.block}) {{")
+                idx = []
+                r_ = "e_"
+                for d in range(s - 1, -1, -1):
+                    if d == 0:
+                        idx.insert(0, f"({r_})")
+                    else:
+                        idx.insert(0, f"(({r_}) % {brick[d]})")
+                        r_ = f"({r_}) / {brick[d]}"
+                addr = " + ".join(f"(lo{d} + {idx[d]}) * {gst[d]}" for d in range(s))
+                B(f"      sg_brick[{l * brick_elems} + e_] = __ldg(G + {addr}); }} }}")
+        for name, ctype, vals in smem:
+            B(f"  for (int i_ = threadIdx.x; i_ < {len(vals)}; i_ += {cfg.block}) {name}[i_] = {name}_c[i_];")
         B("  __syncthreads();")
-    B(f"  const long long qi = (long long)blockIdx.x * {cfg.block} + threadIdx.x;")
-    B("  if (qi >= n) return;")
-    for d in range(s):
-        B(f"  const double x{d} = (double)xs[qi * {s} + {d}];")
-    B(f"  {T} acc = ({T})0;")
+        if cfg.stage == "tma":
+            B('  asm volatile("{\\n .reg .pred p;\\n SG_WAIT_%=:\\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\\n @!p bra SG_WAIT_%=;\\n}" :: "r"(sg_bar_a) : "memory");')
+        B("  const int q_end = starts[bin + 1];")
+        B(f"  for (int qq = starts[bin] + threadIdx.x; qq < q_end; qq += {cfg.block}) {{")
+        B("  const float4 q4 = sorted[qq];")
+        B("  const long long qi = (long long)__float_as_int(q4.w);")
+        comps = ["x", "y", "z"]
+        for d in range(s):
+            B(f"  const double x{d} = (double)q4.{comps[d]};")
+        # coset-0 shift and its wrap -> brick-relative offset rel_d (loc = k + rel)
+        rnd0 = rm0.rounding if rm0.shape == PARALLELEPIPED else ROUND_NEAREST
+        for d in range(s):
+            if rnd0 == ROUND_NEAREST:
+                B(f"  const long long kb{d} = (long long)(x{d} >= 0.0 ? floor(__dadd_rn(x{d}, 0.5)) : ceil(__dsub_rn(x{d}, 0.5)));")
+            else:
+                B(f"  const long long kb{d} = (long long)floor(x{d});")
+            e_ = ext[0][d]
+            B(f"  long long kbw{d} = kb{d} % {e_}LL; if (kbw{d} < 0) kbw{d} += {e_}LL;")
+            B(f"  const long long rel{d} = kbw{d} - lo{d} + {1 + h} - kb{d};")
+        ind = "  "
+    B(f"{ind}{T} acc = ({T})0;")
     if cfg.grad:
         for d in range(s):
-            B(f"  {T} gacc{d} = ({T})0;")
+            B(f"{ind}{T} gacc{d} = ({T})0;")
     em.lines = []
 
     def emit_coset(l, dyn):
         """Body for coset `l` (int) or the loop variable `l` (dyn=True)."""
         L = em.line
         if dyn:
-            ptr = f"(const {T}*)vol.base[0]"
-            for c in range(1, M):
-                ptr = f"(l == {c} ? (const {T}*)vol.base[{c}] : {ptr})"
-            L(f"const {T}* __restrict__ V = {ptr};")
+            if binned:
+                L(f"const float* V = sg_brick + l * {brick_elems};")
+            else:
+                ptr = f"(const {T}*)vol.base[0]"
+                for c in range(1, M):
+                    ptr = f"(l == {c} ? (const {T}*)vol.base[{c}] : {ptr})"
+                L(f"const {T}* __restrict__ V = {ptr};")
             for d in range(s):
                 offs = [float(t.cosets[c][d]) for c in range(M)]
                 if all(o == 0.0 for o in offs):
@@ -489,7 +615,10 @@ def generate(space, config: GenConfig | None = None, extents=None,
                         expr = f"(l == {c} ? {dlit(t.cosets[c][d])} : {expr})"
                     L(f"const double xl{d} = __dsub_rn(x{d}, {expr});")
         else:
-            L(f"const {T}* __restrict__ V = (const {T}*)vol.base[{l}];")
+            if binned:
+                L(f"const float* V = sg_brick + {l * brick_elems};")
+            else:
+                L(f"const {T}* __restrict__ V = (const {T}*)vol.base[{l}];")
             for d in range(s):
                 o = t.cosets[l][d]
                 if o == 0:
@@ -570,10 +699,14 @@ def generate(space, config: GenConfig | None = None, extents=None,
             raise ValueError("rolled coset loop needs equal coset extents")
         e_ = ext[geo]
         st_ = strides[geo]
-        for d in range(s):
-            L(f"int kw{d} = (int)k{d};")
-            L(f"if ((unsigned)kw{d} >= {e_[d]}u) {{ long long m_ = k{d} % {e_[d]}LL; "
-              f"kw{d} = (int)(m_ < 0 ? m_ + {e_[d]}LL : m_); }}")
+        if binned:
+            for d in range(s):
+                L(f"const int kw{d} = (int)(k{d} + rel{d});")
+        else:
+            for d in range(s):
+                L(f"int kw{d} = (int)k{d};")
+                L(f"if ((unsigned)kw{d} >= {e_[d]}u) {{ long long m_ = k{d} % {e_[d]}LL; "
+                  f"kw{d} = (int)(m_ < 0 ? m_ + {e_[d]}LL : m_); }}")
         L("const int base = " + " + ".join(
             f"kw{d} * {st_[d]}" if st_[d] != 1 else f"kw{d}" for d in range(s)) + ";")
         # ---- per-sub fetch offsets
@@ -658,7 +791,10 @@ def generate(space, config: GenConfig | None = None, extents=None,
             for step in plan.steps:
                 if step.kind == FETCH:
                     j = step.index
-                    L(f"const {T} c{j}{tag} = __ldg(V + ({off_expr(j)}));")
+                    if binned:
+                        L(f"const {T} c{j}{tag} = V[{off_expr(j)}];")
+                    else:
+                        L(f"const {T} c{j}{tag} = __ldg(V + ({off_expr(j)}));")
                 elif step.kind == COMPUTE:
                     if u is None or refetch:
                         u = emit_u(f"{tag}_{nchunk}" if refetch else tag)
@@ -757,6 +893,8 @@ def generate(space, config: GenConfig | None = None, extents=None,
     if cfg.grad:
         for d in range(s):
             body.append(f"  grad[qi * {s} + {d}] = gacc{d};")
+    if binned:
+        body.append("  }")
     body.append("}")
     if lut:
         lit = ", ".join(flit(Fraction(v), fw) for v in lut)
@@ -764,7 +902,10 @@ def generate(space, config: GenConfig | None = None, extents=None,
     src = "\n".join(head + body) + "\n"
     return CudaProgram(
         name=space.name, source=src, entry=ENTRY, dim=s, ncosets=M, float_width=fw,
-        block=cfg.block, halo=h, extents=ext, padded_extents=pext, has_grad=cfg.grad,
+        block=cfg.block, halo=H, extents=ext, padded_extents=pext, has_grad=cfg.grad,
         has_dbg=cfg.dbg, config=cfg, space=space,
-        meta={"fetch_mode": fetch_mode, "K": t.K, "nsub": t.nsub, "n": t.n,
+        mode=cfg.mode, bin=bin_ if binned else 0, brick=tuple(brick) if binned else (),
+        smem_bytes=smem_bytes if binned else 0, stage_tma=binned and cfg.stage == "tma",
+        rounding=(0 if (rm0.shape == PARALLELEPIPED and rm0.rounding == "floor") else 1),
+        meta={"fetch_mode": fetch_mode, "K": t.K, "nsub": t.nsub, "n": t.n, "reach": h,
               "smem_tables": [x[0] for x in smem], "lut_entries": len(lut)})

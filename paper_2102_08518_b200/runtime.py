@@ -43,7 +43,11 @@ class sg_module_info(ctypes.Structure):
                 ("block", ctypes.c_int32), ("has_grad", ctypes.c_int32),
                 ("has_dbg", ctypes.c_int32), ("halo", ctypes.c_int32),
                 ("queries_per_thread", ctypes.c_int32),
-                ("padded_extents", (ctypes.c_int64 * SG_MAX_DIM) * SG_MAX_COSETS)]
+                ("padded_extents", (ctypes.c_int64 * SG_MAX_DIM) * SG_MAX_COSETS),
+                ("mode", ctypes.c_int32), ("rounding", ctypes.c_int32),
+                ("stage_tma", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
+                ("bin", ctypes.c_int32), ("brick", ctypes.c_int32 * SG_MAX_DIM),
+                ("extents", ctypes.c_int64 * SG_MAX_DIM)]
 
 
 _lib = None
@@ -66,8 +70,9 @@ EXPORTS = {
     "sg_module_status": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint32)],
                          ctypes.c_int),
     "sg_volume_create": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64),
-                          ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int,
-                          ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+                          ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_int,
+                          ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, ctypes.c_void_p,
+                          ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
     "sg_volume_free": ([ctypes.c_void_p], ctypes.c_int),
     "sg_volume_bytes": ([ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
     "sg_volume_coset_ptr": ([ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)],
@@ -176,6 +181,15 @@ class Module:
         for c, row in enumerate(prog.padded_extents):
             for d, e in enumerate(row):
                 info.padded_extents[c][d] = e
+        info.mode = 1 if prog.mode == "binned" else 0
+        info.rounding = prog.rounding
+        info.stage_tma = int(prog.stage_tma)
+        info.smem_bytes = prog.smem_bytes
+        info.bin = prog.bin
+        for d, e in enumerate(prog.brick):
+            info.brick[d] = e
+        for d, e in enumerate(prog.extents[0]):
+            info.extents[d] = e
         h = ctypes.c_void_p()
         buf = ctypes.create_string_buffer(self.image, len(self.image))
         _check(lib().sg_module_load(buf, len(self.image), prog.entry.encode(), device,
@@ -202,7 +216,7 @@ class Module:
 class Volume:
     """Coset arrays on the device with a periodic ghost halo (sg_volume)."""
 
-    def __init__(self, arrays, halo: int, dtype, device: int = 0, stream=None):
+    def __init__(self, arrays, halo: int, dtype, device: int = 0, stream=None, padded=None):
         import torch
         arrs = list(arrays)
         if not arrs:
@@ -229,7 +243,10 @@ class Volume:
                 keep.append(np.ascontiguousarray(a, dtype=np_dtype))
             ptrs = (ctypes.c_void_p * len(arrs))(*[k.ctypes.data for k in keep])
         h = ctypes.c_void_p()
-        _check(lib().sg_volume_create(device, self.dim, len(arrs), ext, halo,
+        pad = None
+        if padded is not None:
+            pad = (ctypes.c_int64 * (len(arrs) * self.dim))(*[e for row in padded for e in row])
+        _check(lib().sg_volume_create(device, self.dim, len(arrs), ext, halo, pad,
                                       SG_F32 if np_dtype == np.float32 else SG_F64, ptrs,
                                       int(on_dev), _stream_ptr(stream), ctypes.byref(h)))
         self.handle = h

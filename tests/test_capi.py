@@ -37,7 +37,7 @@ def test_invalid_arguments_fail_without_gpu():
     import ctypes
     lib = runtime.lib()
     h = ctypes.c_void_p()
-    rc = lib.sg_volume_create(0, 9, 1, None, 0, 0, None, 0, None, ctypes.byref(h))
+    rc = lib.sg_volume_create(0, 9, 1, None, 0, None, 0, None, 0, None, ctypes.byref(h))
     assert rc == runtime.SG_EINVAL
     rc = lib.sg_eval(None, None, None, 0, None, None, None, None)
     assert rc == runtime.SG_EINVAL

@@ -37,9 +37,10 @@ def _xs(z, which, dtype=torch.float32):
 
 
 @pytest.mark.parametrize("name", golden_names())
-def test_selection_bit_exact(name):
+@pytest.mark.parametrize("mode", ["direct", "binned"])
+def test_selection_bit_exact(name, mode):
     space, _, z, arrays = load_golden(name)
-    ev = _evaluator(space, arrays, dbg=True)
+    ev = _evaluator(space, arrays, dbg=True, mode=mode)
     for which in SETS:
         out, _, dbg = ev(_xs(z, which))
         dbg = dbg.cpu().numpy()
@@ -60,6 +61,9 @@ CONFIGS = [
     dict(params_md=(2, 4)),
     dict(params_md=(2, 4), refetch=True),
     dict(block=256),
+    dict(mode="binned"),
+    dict(mode="binned", stage="ldg", unroll_cosets=False),
+    dict(mode="binned", form="sites", block=256),
 ]
 
 
@@ -100,12 +104,13 @@ def test_values_f64_variant(name):
 
 
 @pytest.mark.parametrize("name", golden_names())
-def test_gradient_vs_oracle(name):
+@pytest.mark.parametrize("mode", ["direct", "binned"])
+def test_gradient_vs_oracle(name, mode):
     space, ospace, z, arrays = load_golden(name)
     xs = z["uniform_xs"].astype(np.float64)
     _, gwant = refeval.reference_eval_batch(ospace, xs, [a.astype(np.float64) for a in arrays],
                                             grad=True)
-    ev = _evaluator(space, arrays, grad=True)
+    ev = _evaluator(space, arrays, grad=True, mode=mode)
     out, g, _ = ev(_xs(z, "uniform"))
     g = g.double().cpu().numpy()
     scale = max(1.0, float(np.abs(gwant).max()))
@@ -113,9 +118,10 @@ def test_gradient_vs_oracle(name):
 
 
 @pytest.mark.parametrize("name", golden_names())
-def test_host_path_matches_device_path(name):
+@pytest.mark.parametrize("mode", ["direct", "binned"])
+def test_host_path_matches_device_path(name, mode):
     space, _, z, arrays = load_golden(name)
-    ev = _evaluator(space, arrays)
+    ev = _evaluator(space, arrays, mode=mode)
     xs = z["uniform_xs"]
     dev = ev(torch.from_numpy(xs).cuda()).cpu().numpy()
     host = ev.eval_host(xs, chunk=257)

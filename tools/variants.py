@@ -1,0 +1,78 @@
+"""Time kernel variants of one benchmark configuration (device time, CUDA events).
+
+    python tools/variants.py c2 [--n 16777216]
+Prints one line per variant: ms per launch, Grecon/s, registers.
+"""
+import argparse
+import itertools
+import json
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2102_08518_b200 import Evaluator, load_fixture  # noqa: E402
+from paper_2102_08518_b200 import runtime  # noqa: E402
+
+VARIANTS = {
+    "direct": dict(mode="direct", block=128),
+    "binned_tma_b256_loop": dict(mode="binned", stage="tma", block=256, unroll_cosets=False),
+    "binned_tma_b256_unroll": dict(mode="binned", stage="tma", block=256, unroll_cosets=True),
+    "binned_ldg_b256_loop": dict(mode="binned", stage="ldg", block=256, unroll_cosets=False),
+    "binned_tma_b128_loop": dict(mode="binned", stage="tma", block=128, unroll_cosets=False),
+    "binned_tma_b512_loop": dict(mode="binned", stage="tma", block=512, unroll_cosets=False),
+    "binned_tma_sites_loop": dict(mode="binned", stage="tma", block=256, unroll_cosets=False, form="sites"),
+    "binned_tma_sites_unroll": dict(mode="binned", stage="tma", block=256, unroll_cosets=True, form="sites"),
+    "binned_tma_bin4": dict(mode="binned", stage="tma", block=128, unroll_cosets=False, bin=4),
+    "binned_tma_bin16": dict(mode="binned", stage="tma", block=512, unroll_cosets=False, bin=16),
+    "binned_tma_lut": dict(mode="binned", stage="tma", block=256, unroll_cosets=False, coeffs="lut"),
+}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("config", nargs="?", default="c2")
+    ap.add_argument("--only", default="")
+    ap.add_argument("--reps", type=int, default=50)
+    a = ap.parse_args()
+    c = bench.CONFIGS[a.config]
+    dev = torch.device("cuda", 0)
+    space, arrays, xs = bench.make_inputs(a.config, 0, dev)
+    n = xs.shape[0]
+    out = torch.empty(n, device=dev)
+    ref = None
+    for name, over in VARIANTS.items():
+        if a.only and a.only not in name:
+            continue
+        try:
+            _, prog = bench.build_program(a.config, **over)
+            ev = Evaluator(space, arrays, prog=prog)
+        except Exception as e:  # noqa: BLE001
+            print(f"{name:28s} FAILED {e}")
+            continue
+        for _ in range(3):
+            runtime.eval_device(ev.module, ev.volume, xs, out)
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(a.reps):
+            runtime.eval_device(ev.module, ev.volume, xs, out)
+        s1.record()
+        torch.cuda.synchronize()
+        ms = s0.elapsed_time(s1) / a.reps
+        ev.module.status()
+        if ref is None:
+            ref = out.clone()
+        diff = float((out - ref).abs().max())
+        print(f"{name:28s} {ms:8.4f} ms  {n / ms / 1e6:8.3f} Grecon/s  regs {ev.module.regs()[0]:3d}"
+              f"  maxdiff-vs-first {diff:.2e}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
