@@ -394,7 +394,8 @@ def generate(space, config: GenConfig | None = None, extents=None,
         for d in range(s - 2, -1, -1):
             bstr[d] = bstr[d + 1] * brick[d + 1]
         brick_elems = bstr[0] * brick[0]
-        smem_bytes = 128 * (-(-(M * brick_elems * 4) // 128))
+        brick_elems = -(-brick_elems // 32) * 32       # 128-B aligned TMA destinations
+        smem_bytes = M * brick_elems * 4
     else:
         H = h
         pext = tuple(tuple(e + 2 * h for e in row) for row in ext)
@@ -543,7 +544,10 @@ def generate(space, config: GenConfig | None = None, extents=None,
             B('    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(sg_bar_a) : "memory");')
             B('    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");')
             B('    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");')
-            B(f'    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(sg_bar_a), "r"({M * brick_elems * 4}) : "memory");')
+            box_bytes = 4
+            for e in brick:
+                box_bytes *= e
+            B(f'    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(sg_bar_a), "r"({M * box_bytes}) : "memory");')
             for l in range(M):
                 B(f"    {{ const unsigned dst = (unsigned)__cvta_generic_to_shared(sg_brick + {l * brick_elems});")
                 B(f'      asm volatile("cp.async.bulk.tensor.{s}d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {{{coords}}}], [%{2 + s}];"')
@@ -551,10 +555,13 @@ def generate(space, config: GenConfig | None = None, extents=None,
             B("  }")
         else:
             bz = brick[-1]
+            box_elems = 1
+            for e in brick:
+                box_elems *= e
             for l in range(M):
                 off0 = sum(H * gst[d] for d in range(s))
                 B(f"  {{ const float* __restrict__ G = (const float*)vol.base[{l}] - {off0};")
-                B(f"    for (int e_ = threadIdx.x; e_ < {brick_elems}; e_ += {cfg.block}) {{")
+                B(f"    for (int e_ = threadIdx.x; e_ < {box_elems}; e_ += {cfg.block}) {{")
                 idx = []
                 r_ = "e_"
                 for d in range(s - 1, -1, -1):

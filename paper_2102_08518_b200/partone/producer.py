@@ -328,7 +328,14 @@ class Producer:
                 raise RuntimeError("fit point left the region")
         return pts
 
-    def fit(self):
+    def fit(self, method="symbolic"):
+        """Per representative region and site: the polynomial of phi(x - n) on the region.
+
+        method "symbolic": run the box-spline recurrence on polynomials (pieces.py);
+        method "interp": exact interpolation on a principal simplex lattice.
+        Either way every piece is certified against exact point values of phi at
+        hold-out points inside the region."""
+        from .pieces import PieceEvaluator, phi_piece
         s = self.s
         deg = self.phi.degree()
         monos = [e for e in itertools.product(range(deg + 1), repeat=s) if sum(e) <= deg]
@@ -336,30 +343,34 @@ class Producer:
         self.ref_polys = []
         self.ref_stencils = []
         norm = self.normalization()
+        pev = PieceEvaluator(s)
         for ri, idx in enumerate(self.reps):
             R = self.region_list[idx]
-            pts = self._fit_points(R, deg)
-            Vm = [[_mono(x, e) for e in monos] for x in pts]
-            lu = _LU(Vm)
             sites = self._candidate_sites(R)
-            kept = []
-            polys = []
-            hold = [self._interior_sample(R) for _ in range(4)]
+            hold = [self._interior_sample(R) for _ in range(3)]
+            kept, polys = [], []
+            lu = pts = None
             for n in sites:
-                vals = [norm * self.phi(exact.sub(x, tuple(F(v) for v in n))) for x in pts]
-                if not any(vals):
+                nv = tuple(F(v) for v in n)
+                if method == "symbolic":
+                    pc = phi_piece(self.phi, pev, R.point, nv)
+                    poly = {e: c * norm for e, c in pc.items() if c}
+                else:
+                    if lu is None:
+                        pts = self._fit_points(R, deg)
+                        lu = _LU([[_mono(x, e) for e in monos] for x in pts])
+                    vals = [norm * self.phi(exact.sub(x, nv)) for x in pts]
+                    coef = lu.solve(vals) if any(vals) else [F(0)] * len(monos)
+                    poly = {e: c for e, c in zip(monos, coef) if c}
+                if not poly:
                     continue
-                coef = lu.solve(vals)
-                if not any(coef):
-                    continue
-                # hold-out verification (exact)
                 for x in hold:
-                    want = norm * self.phi(exact.sub(x, tuple(F(v) for v in n)))
-                    got = sum(c * _mono(x, e) for c, e in zip(coef, monos))
+                    want = norm * self.phi(exact.sub(x, nv))
+                    got = sum(c * _mono(x, e) for e, c in poly.items())
                     if got != want:
-                        raise RuntimeError(f"fit failed hold-out check at site {n}")
+                        raise RuntimeError(f"piece of site {n} fails the hold-out check")
                 kept.append(tuple(int(v) for v in n))
-                polys.append(dict((e, c) for e, c in zip(monos, coef) if c))
+                polys.append(poly)
             order = sorted(range(len(kept)), key=lambda i: kept[i])
             kept = [kept[i] for i in order]
             polys = [polys[i] for i in order]
