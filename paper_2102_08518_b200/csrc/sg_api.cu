@@ -134,40 +134,40 @@ __global__ void sg_pad_kernel(T* __restrict__ dst, const T* __restrict__ src, in
 }
 
 
-// ---- binned mode: counting sort of the queries by coset-0 lattice cell ------------------
+// ---- binned mode: counting sort of the queries by cell ---------------------------------
 //
-// The bin of a query is computed from k0 = rho(x) of coset 0 (offset 0, identity basis),
-// with exactly the fp64 operations the generated kernel uses, so both agree on k0.
+// Bins partition the periodic box of coset 0 into cubes of `bin` cells.  The bin of a
+// query is computed in cheap f32 arithmetic from the wrapped coordinate; the generated
+// kernel recomputes the exact fp64 lattice shift and tolerates a one-cell disagreement
+// at bin borders (its brick carries a margin of reach + 2 cells, and the brick-local
+// index is wrapped modulo the extent), so bins only need to be *approximately* right.
 struct BinGeom {
-  int dim, rounding, bin;
-  long long ext[3];
-  long long nb[3];
+  int dim, bin;
+  float ext[3];
+  float inv_ext[3];
+  float inv_bin;
+  int nb[3];
   long long nbins;
 };
 
-__device__ __forceinline__ long long sg_rho0(double x, int rounding) {
-  if (rounding == SG_ROUND)
-    return (long long)(x >= 0.0 ? floor(__dadd_rn(x, 0.5)) : ceil(__dsub_rn(x, 0.5)));
-  return (long long)floor(x);
-}
-
 __device__ __forceinline__ int sg_bin_of(const float* __restrict__ xs, long long i,
                                          const BinGeom& g) {
-  long long lin = 0;
+  int lin = 0;
   for (int d = 0; d < g.dim; ++d) {
-    long long k = sg_rho0((double)xs[i * g.dim + d], g.rounding);
-    long long kw = k % g.ext[d];
-    if (kw < 0) kw += g.ext[d];
-    lin = lin * g.nb[d] + kw / g.bin;
+    float x = xs[i * g.dim + d];
+    float xw = x - g.ext[d] * floorf(x * g.inv_ext[d]);   // wrap into [0, E) (approximately)
+    int b = (int)floorf(xw * g.inv_bin);
+    b = min(max(b, 0), g.nb[d] - 1);
+    lin = lin * g.nb[d] + b;
   }
-  return (int)lin;
+  return lin;
 }
 
-constexpr int SG_BIN_CHUNK = 4096;      // queries per histogram / scatter CTA
-constexpr int SG_SMEM_BINS = 12288;     // bins that fit a privatized shared histogram
+constexpr int SG_BIN_CHUNK = 16384;     // queries per histogram / scatter CTA
+constexpr int SG_SMEM_BINS = 24576;     // bins that fit a privatized shared histogram
 
-__global__ void sg_bin_count(const float* __restrict__ xs, long long n, BinGeom g,
-                             int* __restrict__ counts) {
+__global__ void __launch_bounds__(1024) sg_bin_count(const float* __restrict__ xs, long long n,
+                                                    BinGeom g, int* __restrict__ counts) {
   extern __shared__ int hist[];
   const bool priv = g.nbins <= SG_SMEM_BINS;
   if (priv)
@@ -214,8 +214,9 @@ __global__ void sg_bin_scan(const int* __restrict__ counts, long long nbins,
   if (t == 1023) starts[nbins] = part[1023];
 }
 
-__global__ void sg_bin_scatter(const float* __restrict__ xs, long long n, BinGeom g,
-                               int* __restrict__ cursors, float4* __restrict__ sorted) {
+__global__ void __launch_bounds__(1024) sg_bin_scatter(const float* __restrict__ xs, long long n,
+                                                      BinGeom g, int* __restrict__ cursors,
+                                                      float4* __restrict__ sorted) {
   extern __shared__ int sh[];
   int* hist = sh;                 // per-CTA counts, then running local offsets
   int* base = sh + SG_SMEM_BINS;  // reserved global position per bin
@@ -598,11 +599,12 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
   int* cursors = starts + nb + 1;
   BinGeom g{};
   g.dim = in.dim;
-  g.rounding = in.rounding;
   g.bin = in.bin;
+  g.inv_bin = 1.0f / (float)in.bin;
   for (int d = 0; d < 3; ++d) {
-    g.ext[d] = d < in.dim ? in.extents[d] : 1;
-    g.nb[d] = d < in.dim ? m->nb[d] : 1;
+    g.ext[d] = d < in.dim ? (float)in.extents[d] : 1.f;
+    g.inv_ext[d] = 1.0f / g.ext[d];
+    g.nb[d] = d < in.dim ? (int)m->nb[d] : 1;
   }
   g.nbins = (long long)nb;
   CU(cudaMemsetAsync(counts, 0, nb * sizeof(int), st));
@@ -618,11 +620,11 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
                          SG_SMEM_BINS * sizeof(int));
     attr_set = true;
   }
-  sg_bin_count<<<(unsigned)chunks, 512, sh1, st>>>((const float*)xs, (long long)n, g, counts);
+  sg_bin_count<<<(unsigned)chunks, 1024, sh1, st>>>((const float*)xs, (long long)n, g, counts);
   CU(cudaGetLastError());
   sg_bin_scan<<<1, 1024, 0, st>>>(counts, (long long)nb, starts, cursors);
   CU(cudaGetLastError());
-  sg_bin_scatter<<<(unsigned)chunks, 512, sh3, st>>>((const float*)xs, (long long)n, g, cursors,
+  sg_bin_scatter<<<(unsigned)chunks, 1024, sh3, st>>>((const float*)xs, (long long)n, g, cursors,
                                                      sorted);
   CU(cudaGetLastError());
   SgCosets cs{};

@@ -382,9 +382,10 @@ def generate(space, config: GenConfig | None = None, extents=None,
             raise ValueError("binned mode needs equal coset extents")
         if any(not (0 <= c < 1) for off in t.cosets for c in off):
             raise ValueError("binned mode needs coset offsets in [0, 1)")
-        H = h + 1
+        margin = h + 2   # f32 binning may be off by one cell; rounding/cosets add one more
+        H = margin
         unit = 4  # TMA: innermost box extent x 4 B must be a multiple of 16 B
-        brick = [bin_ + 2 * h + 2] * s
+        brick = [bin_ + 2 * margin] * s
         brick[-1] = -(-brick[-1] // unit) * unit
         nb = [-(-e // bin_) for e in ext[0]]
         prow = [max(ext[0][d] + 2 * H, (nb[d] - 1) * bin_ + brick[d]) for d in range(s)]
@@ -584,7 +585,8 @@ def generate(space, config: GenConfig | None = None, extents=None,
         comps = ["x", "y", "z"]
         for d in range(s):
             B(f"  const double x{d} = (double)q4.{comps[d]};")
-        # coset-0 shift and its wrap -> brick-relative offset rel_d (loc = k + rel)
+        # coset-0 shift, wrapped, relative to the (approximately assigned) bin:
+        # loc = k + rel lands in [0, brick) for every coset and stencil site
         rnd0 = rm0.rounding if rm0.shape == PARALLELEPIPED else ROUND_NEAREST
         for d in range(s):
             if rnd0 == ROUND_NEAREST:
@@ -592,8 +594,11 @@ def generate(space, config: GenConfig | None = None, extents=None,
             else:
                 B(f"  const long long kb{d} = (long long)floor(x{d});")
             e_ = ext[0][d]
-            B(f"  long long kbw{d} = kb{d} % {e_}LL; if (kbw{d} < 0) kbw{d} += {e_}LL;")
-            B(f"  const long long rel{d} = kbw{d} - lo{d} + {1 + h} - kb{d};")
+            B(f"  int kbw{d} = (int)kb{d};")
+            B(f"  if ((unsigned)kbw{d} >= {e_}u) {{ long long m_ = kb{d} % {e_}LL; kbw{d} = (int)(m_ < 0 ? m_ + {e_}LL : m_); }}")
+            B(f"  int u{d}_ = kbw{d} - lo{d};")
+            B(f"  if (u{d}_ < -1) u{d}_ += {e_}; else if (u{d}_ > {bin_}) u{d}_ -= {e_};")
+            B(f"  const long long rel{d} = (long long)(u{d}_ + {margin}) - kb{d};")
         ind = "  "
     B(f"{ind}{T} acc = ({T})0;")
     if cfg.grad:

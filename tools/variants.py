@@ -22,16 +22,15 @@ from paper_2102_08518_b200 import runtime  # noqa: E402
 
 VARIANTS = {
     "direct": dict(mode="direct", block=128),
-    "binned_tma_b256_loop": dict(mode="binned", stage="tma", block=256, unroll_cosets=False),
-    "binned_tma_b256_unroll": dict(mode="binned", stage="tma", block=256, unroll_cosets=True),
-    "binned_ldg_b256_loop": dict(mode="binned", stage="ldg", block=256, unroll_cosets=False),
-    "binned_tma_b128_loop": dict(mode="binned", stage="tma", block=128, unroll_cosets=False),
-    "binned_tma_b512_loop": dict(mode="binned", stage="tma", block=512, unroll_cosets=False),
-    "binned_tma_sites_loop": dict(mode="binned", stage="tma", block=256, unroll_cosets=False, form="sites"),
-    "binned_tma_sites_unroll": dict(mode="binned", stage="tma", block=256, unroll_cosets=True, form="sites"),
-    "binned_tma_bin4": dict(mode="binned", stage="tma", block=128, unroll_cosets=False, bin=4),
-    "binned_tma_bin16": dict(mode="binned", stage="tma", block=512, unroll_cosets=False, bin=16),
-    "binned_tma_lut": dict(mode="binned", stage="tma", block=256, unroll_cosets=False, coeffs="lut"),
+    "binned_b8_t256_loop": dict(mode="binned", stage="tma", block=256, unroll_cosets=False, bin=8),
+    "binned_b8_t256_unroll": dict(mode="binned", stage="tma", block=256, unroll_cosets=True, bin=8),
+    "binned_b6_t256_loop": dict(mode="binned", stage="tma", block=256, unroll_cosets=False, bin=6),
+    "binned_b4_t128_loop": dict(mode="binned", stage="tma", block=128, unroll_cosets=False, bin=4),
+    "binned_b4_t128_unroll": dict(mode="binned", stage="tma", block=128, unroll_cosets=True, bin=4),
+    "binned_b4_t256_loop": dict(mode="binned", stage="tma", block=256, unroll_cosets=False, bin=4),
+    "binned_b4_ldg_t128": dict(mode="binned", stage="ldg", block=128, unroll_cosets=False, bin=4),
+    "binned_b4_sites_t128": dict(mode="binned", stage="tma", block=128, unroll_cosets=False, bin=4, form="sites"),
+    "binned_b4_sites_unroll": dict(mode="binned", stage="tma", block=128, unroll_cosets=True, bin=4, form="sites"),
 }
 
 
