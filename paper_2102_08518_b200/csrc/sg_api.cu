@@ -163,82 +163,132 @@ __device__ __forceinline__ int sg_bin_of(const float* __restrict__ xs, long long
   return lin;
 }
 
-constexpr int SG_BIN_CHUNK = 16384;     // queries per histogram / scatter CTA
-constexpr int SG_SMEM_BINS = 24576;     // bins that fit a privatized shared histogram
+constexpr int SG_SORT_THREADS = 1024;
+constexpr int SG_SMEM_BINS = 24576;     // bins that fit the privatized shared histograms
+constexpr int SG_SCAN_TILE = 8192;      // elements per CTA in the device-wide scan
 
-__global__ void __launch_bounds__(1024) sg_bin_count(const float* __restrict__ xs, long long n,
-                                                    BinGeom g, int* __restrict__ counts) {
+// K1: per-CTA histogram of a contiguous query range -> mat[bin * G + cta] (no atomics
+// on global memory; the (bin, cta) matrix is scanned bin-major next).
+__global__ void __launch_bounds__(SG_SORT_THREADS) sg_bin_count(
+    const float* __restrict__ xs, long long n, long long per, BinGeom g,
+    int* __restrict__ mat) {
   extern __shared__ int hist[];
-  const bool priv = g.nbins <= SG_SMEM_BINS;
-  if (priv)
-    for (int b = threadIdx.x; b < g.nbins; b += blockDim.x) hist[b] = 0;
+  const int G = gridDim.x;
+  for (int b = threadIdx.x; b < g.nbins; b += blockDim.x) hist[b] = 0;
   __syncthreads();
-  const long long lo = (long long)blockIdx.x * SG_BIN_CHUNK;
-  const long long hi = min(n, lo + SG_BIN_CHUNK);
-  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-    int b = sg_bin_of(xs, i, g);
-    if (priv)
-      atomicAdd(&hist[b], 1);
-    else
-      atomicAdd(&counts[b], 1);
-  }
+  const long long lo = (long long)blockIdx.x * per;
+  const long long hi = min(n, lo + per);
+  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x)
+    atomicAdd(&hist[sg_bin_of(xs, i, g)], 1);
   __syncthreads();
-  if (priv)
-    for (int b = threadIdx.x; b < g.nbins; b += blockDim.x)
-      if (hist[b]) atomicAdd(&counts[b], hist[b]);
+  for (int b = threadIdx.x; b < g.nbins; b += blockDim.x) mat[(long long)b * G + blockIdx.x] = hist[b];
 }
 
-// exclusive scan of counts -> starts[0..nbins], cursors = starts (one CTA of 1024)
-__global__ void sg_bin_scan(const int* __restrict__ counts, long long nbins,
-                            int* __restrict__ starts, int* __restrict__ cursors) {
-  __shared__ int part[1024];
-  const int t = threadIdx.x;
-  const long long per = (nbins + 1023) / 1024;
-  const long long lo = t * per, hi = min(nbins, lo + per);
+// device-wide exclusive scan of `len` ints (3 phases: tile sums, scan of sums, rescan)
+__global__ void __launch_bounds__(1024) sg_scan_tiles(const int* __restrict__ in, long long len,
+                                                      int* __restrict__ tile_sums) {
+  __shared__ int red[32];
+  const long long base = (long long)blockIdx.x * SG_SCAN_TILE;
   int sum = 0;
-  for (long long b = lo; b < hi; ++b) sum += counts[b];
-  part[t] = sum;
+  for (int k = threadIdx.x; k < SG_SCAN_TILE; k += 1024) {
+    long long i = base + k;
+    if (i < len) sum += in[i];
+  }
+  for (int o = 16; o; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
   __syncthreads();
-  for (int off = 1; off < 1024; off <<= 1) {
-    int v = t >= off ? part[t - off] : 0;
-    __syncthreads();
-    part[t] += v;
-    __syncthreads();
+  if (threadIdx.x < 32) {
+    int v = red[threadIdx.x];
+    for (int o = 16; o; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) tile_sums[blockIdx.x] = v;
   }
-  int run = part[t] - sum;  // exclusive prefix of this thread's slice
-  for (long long b = lo; b < hi; ++b) {
-    starts[b] = run;
-    cursors[b] = run;
-    run += counts[b];
-  }
-  if (t == 1023) starts[nbins] = part[1023];
 }
 
-__global__ void __launch_bounds__(1024) sg_bin_scatter(const float* __restrict__ xs, long long n,
-                                                      BinGeom g, int* __restrict__ cursors,
-                                                      float4* __restrict__ sorted) {
-  extern __shared__ int sh[];
-  int* hist = sh;                 // per-CTA counts, then running local offsets
-  int* base = sh + SG_SMEM_BINS;  // reserved global position per bin
-  const bool priv = g.nbins <= SG_SMEM_BINS;
-  const long long lo = (long long)blockIdx.x * SG_BIN_CHUNK;
-  const long long hi = min(n, lo + SG_BIN_CHUNK);
-  if (priv) {
-    for (int b = threadIdx.x; b < g.nbins; b += blockDim.x) hist[b] = 0;
-    __syncthreads();
-    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x)
-      atomicAdd(&hist[sg_bin_of(xs, i, g)], 1);
-    __syncthreads();
-    for (int b = threadIdx.x; b < g.nbins; b += blockDim.x) {
-      int c = hist[b];
-      base[b] = c ? atomicAdd(&cursors[b], c) : 0;
-      hist[b] = 0;
-    }
-    __syncthreads();
+__device__ __forceinline__ int sg_block_excl_scan(int v, int* sh, int* total) {
+  // 1024-thread exclusive scan via warp shuffles
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
   }
+  if (lane == 31) sh[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int t = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    sh[lane] = t;
+  }
+  __syncthreads();
+  int excl = x - v + (w ? sh[w - 1] : 0);
+  if (total) *total = sh[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return excl;
+}
+
+__global__ void __launch_bounds__(1024) sg_scan_sums(int* __restrict__ tile_sums, long long ntiles) {
+  __shared__ int sh[32];
+  int carry = 0;
+  for (long long b = 0; b < ntiles; b += 1024) {
+    long long i = b + threadIdx.x;
+    int v = i < ntiles ? tile_sums[i] : 0;
+    int tot;
+    int e = sg_block_excl_scan(v, sh, &tot);
+    if (i < ntiles) tile_sums[i] = e + carry;
+    carry += tot;
+  }
+}
+
+__global__ void __launch_bounds__(1024) sg_scan_apply(int* __restrict__ data, long long len,
+                                                      const int* __restrict__ tile_offs) {
+  __shared__ int sh[32];
+  const long long base = (long long)blockIdx.x * SG_SCAN_TILE;
+  int carry = tile_offs[blockIdx.x];
+  constexpr int PER = SG_SCAN_TILE / 1024;   // contiguous elements per thread
+  int v[PER];
+  int local = 0;
+  for (int k = 0; k < PER; ++k) {
+    long long i = base + (long long)threadIdx.x * PER + k;
+    v[k] = i < len ? data[i] : 0;
+    local += v[k];
+  }
+  int excl = sg_block_excl_scan(local, sh, nullptr) + carry;
+  for (int k = 0; k < PER; ++k) {
+    long long i = base + (long long)threadIdx.x * PER + k;
+    if (i < len) data[i] = excl;
+    excl += v[k];
+  }
+}
+
+// starts[bin] = offset of (bin, cta 0); starts[nbins] = n
+__global__ void sg_bin_starts(const int* __restrict__ mat, long long nbins, int G, long long n,
+                              int* __restrict__ starts) {
+  long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (b < nbins) starts[b] = mat[b * G];
+  if (b == nbins) starts[b] = (int)n;
+}
+
+// K3: scatter (x, y, z, index) records to their sorted positions
+__global__ void __launch_bounds__(SG_SORT_THREADS) sg_bin_scatter(
+    const float* __restrict__ xs, long long n, long long per, BinGeom g,
+    const int* __restrict__ mat, float4* __restrict__ sorted) {
+  extern __shared__ int sh[];
+  int* base = sh;
+  int* cnt = sh + g.nbins;
+  const int G = gridDim.x;
+  for (int b = threadIdx.x; b < g.nbins; b += blockDim.x) {
+    base[b] = mat[(long long)b * G + blockIdx.x];
+    cnt[b] = 0;
+  }
+  __syncthreads();
+  const long long lo = (long long)blockIdx.x * per;
+  const long long hi = min(n, lo + per);
   for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     int b = sg_bin_of(xs, i, g);
-    int pos = priv ? base[b] + atomicAdd(&hist[b], 1) : atomicAdd(&cursors[b], 1);
+    int pos = base[b] + atomicAdd(&cnt[b], 1);
     float4 r;
     r.x = xs[i * g.dim];
     r.y = g.dim > 1 ? xs[i * g.dim + 1] : 0.f;
@@ -585,7 +635,16 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
   const sg_module_info& in = m->info;
   std::lock_guard<std::mutex> lock(m->bin_mu);
   const size_t nb = (size_t)m->nbins;
-  const size_t need = (size_t)n * sizeof(float4) + (3 * nb + 1) * sizeof(int) + 256;
+  if (nb > (size_t)SG_SMEM_BINS)
+    return fail(SG_EINVAL, "%zu bins exceed the %d supported by the binning kernels; use a larger bin",
+                nb, SG_SMEM_BINS);
+  int dev_sms = 148;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, m->device);
+  const long long G = std::max<long long>(1, std::min<long long>((n + 8191) / 8192, 8LL * dev_sms));
+  const long long per = (n + G - 1) / G;
+  const long long mlen = (long long)nb * G;
+  const long long ntiles = (mlen + SG_SCAN_TILE - 1) / SG_SCAN_TILE;
+  const size_t need = (size_t)n * sizeof(float4) + ((size_t)mlen + ntiles + nb + 1) * sizeof(int) + 512;
   if (m->bin_scratch_bytes < need) {
     if (m->bin_scratch) cudaFree(m->bin_scratch);
     m->bin_scratch = nullptr;
@@ -594,9 +653,9 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
     m->bin_scratch_bytes = need;
   }
   float4* sorted = (float4*)m->bin_scratch;
-  int* counts = (int*)(sorted + n);
-  int* starts = counts + nb;
-  int* cursors = starts + nb + 1;
+  int* mat = (int*)(sorted + n);
+  int* tile_sums = mat + mlen;
+  int* starts = tile_sums + ntiles;
   BinGeom g{};
   g.dim = in.dim;
   g.bin = in.bin;
@@ -607,25 +666,24 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
     g.nb[d] = d < in.dim ? (int)m->nb[d] : 1;
   }
   g.nbins = (long long)nb;
-  CU(cudaMemsetAsync(counts, 0, nb * sizeof(int), st));
-  const long long chunks = (n + SG_BIN_CHUNK - 1) / SG_BIN_CHUNK;
-  const bool priv = nb <= (size_t)SG_SMEM_BINS;
-  size_t sh1 = priv ? nb * sizeof(int) : 0;
-  size_t sh3 = priv ? 2 * SG_SMEM_BINS * sizeof(int) : 0;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [] {
     cudaFuncSetAttribute(sg_bin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          2 * SG_SMEM_BINS * sizeof(int));
     cudaFuncSetAttribute(sg_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          SG_SMEM_BINS * sizeof(int));
-    attr_set = true;
-  }
-  sg_bin_count<<<(unsigned)chunks, 1024, sh1, st>>>((const float*)xs, (long long)n, g, counts);
+  });
+  sg_bin_count<<<(unsigned)G, SG_SORT_THREADS, nb * sizeof(int), st>>>((const float*)xs, (long long)n,
+                                                                      per, g, mat);
   CU(cudaGetLastError());
-  sg_bin_scan<<<1, 1024, 0, st>>>(counts, (long long)nb, starts, cursors);
+  sg_scan_tiles<<<(unsigned)ntiles, 1024, 0, st>>>(mat, mlen, tile_sums);
+  sg_scan_sums<<<1, 1024, 0, st>>>(tile_sums, ntiles);
+  sg_scan_apply<<<(unsigned)ntiles, 1024, 0, st>>>(mat, mlen, tile_sums);
+  sg_bin_starts<<<(unsigned)((nb + 256) / 256), 256, 0, st>>>(mat, (long long)nb, (int)G, (long long)n,
+                                                              starts);
   CU(cudaGetLastError());
-  sg_bin_scatter<<<(unsigned)chunks, 1024, sh3, st>>>((const float*)xs, (long long)n, g, cursors,
-                                                     sorted);
+  sg_bin_scatter<<<(unsigned)G, SG_SORT_THREADS, 2 * nb * sizeof(int), st>>>(
+      (const float*)xs, (long long)n, per, g, mat, sorted);
   CU(cudaGetLastError());
   SgCosets cs{};
   for (int c = 0; c < v->ncosets; ++c) cs.base[c] = v->origin[c];

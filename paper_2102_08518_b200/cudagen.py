@@ -388,6 +388,11 @@ def generate(space, config: GenConfig | None = None, extents=None,
         brick = [bin_ + 2 * margin] * s
         brick[-1] = -(-brick[-1] // unit) * unit
         nb = [-(-e // bin_) for e in ext[0]]
+        while int(np.prod(nb)) > 24576:        # the binning kernels' shared histogram limit
+            bin_ += 2
+            nb = [-(-e // bin_) for e in ext[0]]
+        brick = [bin_ + 2 * margin] * s
+        brick[-1] = -(-brick[-1] // unit) * unit
         prow = [max(ext[0][d] + 2 * H, (nb[d] - 1) * bin_ + brick[d]) for d in range(s)]
         prow[-1] = -(-prow[-1] // unit) * unit
         pext = tuple(tuple(prow) for _ in range(M))
