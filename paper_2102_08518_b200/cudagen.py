@@ -44,7 +44,7 @@ F64 = "f64"
 F32 = "f32"
 ENTRY = "sg_eval_kernel"
 FORMS = ("horner", "sites")
-COEFFS = ("imm", "lut")
+COEFFS = ("imm", "lut", "table")
 
 
 @dataclass(frozen=True)
@@ -385,16 +385,15 @@ def generate(space, config: GenConfig | None = None, extents=None,
         margin = h + 2   # f32 binning may be off by one cell; rounding/cosets add one more
         H = margin
         unit = 4  # TMA: innermost box extent x 4 B must be a multiple of 16 B
-        brick = [bin_ + 2 * margin] * s
-        brick[-1] = -(-brick[-1] // unit) * unit
         nb = [-(-e // bin_) for e in ext[0]]
         while int(np.prod(nb)) > 24576:        # the binning kernels' shared histogram limit
             bin_ += 2
             nb = [-(-e // bin_) for e in ext[0]]
-        brick = [bin_ + 2 * margin] * s
-        brick[-1] = -(-brick[-1] // unit) * unit
+        # TMA boxes: every extent a multiple of 4 elements (measured: boxes with 13/14-wide
+        # outer dims fault on sm_100a), padded global extents multiples of 16
+        brick = [-(-(bin_ + 2 * margin) // unit) * unit] * s
         prow = [max(ext[0][d] + 2 * H, (nb[d] - 1) * bin_ + brick[d]) for d in range(s)]
-        prow[-1] = -(-prow[-1] // unit) * unit
+        prow = [-(-v // 16) * 16 for v in prow]
         pext = tuple(tuple(prow) for _ in range(M))
         bstr = [1] * s
         for d in range(s - 2, -1, -1):
@@ -479,6 +478,27 @@ def generate(space, config: GenConfig | None = None, extents=None,
             smem.append((f"sg_off{g}", "int", vals))
     if not t.uniform_psi and t.K > 1:
         smem.append(("sg_psi", "int", list(t.psi)))
+    tab = None
+    if cfg.coeffs == "table":
+        # monomial-major lookup table: A[psi][j][m] = coefficient of u^e_m c_j in psi
+        exps = sorted({e for rp in space.ref_polys for (e, _c) in rp.poly.terms})
+        nm = len(exps)
+        nmp = -(-nm // 4) * 4
+        midx = {e: i for i, e in enumerate(exps)}
+        Atab = [0.0] * (t.K * t.n * nmp)
+        A0tab = [0.0] * (t.K * nmp)
+        for k_, rp in enumerate(space.ref_polys):
+            for (e, c), q in rp.poly.terms.items():
+                if c == NO_SYMBOL:
+                    A0tab[k_ * nmp + midx[e]] = q
+                else:
+                    Atab[(k_ * t.n + c) * nmp + midx[e]] = q
+        tab = dict(exps=exps, nm=nm, nmp=nmp, has_free=any(v != 0 for v in A0tab))
+        smem.append(("sg_A", T, Atab))
+        if tab["has_free"]:
+            smem.append(("sg_A0", T, A0tab))
+        if 4 * len(Atab) > 96 * 1024:
+            raise ValueError("coefficient table too large for shared memory")
 
     lut = []
     if cfg.coeffs == "lut":
@@ -511,7 +531,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
         B(f"    const {T}* __restrict__ xs, long long n, {T}* __restrict__ out, {T}* __restrict__ grad,")
         B("    int* __restrict__ dbg, unsigned* __restrict__ err, SgCosets vol) {")
         for name, ctype, vals in smem:
-            B(f"  __shared__ {ctype} {name}[{len(vals)}];")
+            B(f"  __shared__ __align__(16) {ctype} {name}[{len(vals)}];")
         for name, ctype, vals in smem:
             B(f"  for (int i_ = threadIdx.x; i_ < {len(vals)}; i_ += {cfg.block}) {name}[i_] = {name}_c[i_];")
         if smem:
@@ -529,7 +549,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
         B("  extern __shared__ __align__(128) float sg_brick[];")
         B("  __shared__ __align__(8) unsigned long long sg_bar;")
         for name, ctype, vals in smem:
-            B(f"  __shared__ {ctype} {name}[{len(vals)}];")
+            B(f"  __shared__ __align__(16) {ctype} {name}[{len(vals)}];")
         # bin coordinates (row-major over nb)
         B("  const int bin = blockIdx.x;")
         rem = "bin"
@@ -856,7 +876,77 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 if parts:
                     L(f"gacc{e} += {' + '.join(parts)};")
 
-        if t.K == 1:
+        def nested_horner(coef, u):
+            """sum_e coef(e) u^e over tab['exps'] by nested Horner (axis 0 outermost).
+            coef(e) returns an operand string or None (absent)."""
+            def rec(fixed, axis):
+                if axis == s:
+                    return coef(tuple(fixed))
+                pows = sorted({e[axis] for e in tab["exps"] if tuple(e[:axis]) == tuple(fixed)})
+                if not pows:
+                    return None
+                r = None
+                for a in range(pows[-1], -1, -1):
+                    q = rec(list(fixed) + [a], axis + 1) if a in pows else None
+                    if r is None:
+                        r = q
+                    else:
+                        nt = em.tmp("h")
+                        if q is None:
+                            L(f"const {T} {nt} = {r} * {u[axis]};")
+                        else:
+                            L(f"const {T} {nt} = {r} * {u[axis]} + {q};")
+                        r = nt
+                return r
+            return rec([], 0) or f"({T})0"
+
+        def run_table():
+            nmp = tab["nmp"]
+            midx = {e: i for i, e in enumerate(tab["exps"])}
+            psi_e = "psi" if t.K > 1 else "0"
+            vec = "float4" if T == "float" else "double2"
+            w = 4 if T == "float" else 2
+            comps = ["x", "y", "z", "w"][:w]
+            L(f"const {vec}* __restrict__ Arow = reinterpret_cast<const {vec}*>(&sg_A[{psi_e} * {t.n * nmp}]);")
+            for m in range(nmp):
+                L(f"{T} g{m} = ({T})0;")
+            u = None
+            nchunk = 0
+            for step in plan.steps:
+                if step.kind == FETCH:
+                    j = step.index
+                    if binned:
+                        L(f"const {T} c{j} = V[{off_expr(j)}];")
+                    else:
+                        L(f"const {T} c{j} = __ldg(V + ({off_expr(j)}));")
+                elif step.kind == COMPUTE:
+                    for j in plan.blocks[step.index]:
+                        for q in range(nmp // w):
+                            L(f"{{ const {vec} a_ = Arow[{(j * nmp) // w + q}]; " + " ".join(
+                                f"g{q * w + r} = a_.{comps[r]} * c{j} + g{q * w + r};" for r in range(w)) + " }")
+                    nchunk += 1
+            if tab["has_free"]:
+                L(f"const {T}* __restrict__ A0row = &sg_A0[{psi_e} * {nmp}];")
+                for m in range(tab["nm"]):
+                    L(f"g{m} += A0row[{m}];")
+            u = emit_u("")
+            val = nested_horner(lambda e: f"g{midx[e]}" if e in midx else None, u)
+            L(f"acc += {val};")
+            if cfg.grad:
+                du = []
+                for a in range(s):
+                    def dcoef(e, a=a):
+                        e2 = tuple(v + (k == a) for k, v in enumerate(e))
+                        if e2 not in midx:
+                            return None
+                        f = e[a] + 1
+                        return f"g{midx[e2]}" if f == 1 else f"{flit(f, fw)} * g{midx[e2]}"
+                    du.append(nested_horner(dcoef, u))
+                add_grad(du, True)
+
+        if cfg.coeffs == "table":
+            run_table()
+        elif t.K == 1:
             accs, grads, _ = run_plan([0], "")
             L(f"acc += {accs[0]};")
             if cfg.grad:

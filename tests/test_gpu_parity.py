@@ -64,6 +64,8 @@ CONFIGS = [
     dict(mode="binned"),
     dict(mode="binned", stage="ldg", unroll_cosets=False),
     dict(mode="binned", form="sites", block=256),
+    dict(coeffs="table"),
+    dict(coeffs="table", mode="binned", params_md=(2, 4)),
 ]
 
 
@@ -104,13 +106,16 @@ def test_values_f64_variant(name):
 
 
 @pytest.mark.parametrize("name", golden_names())
-@pytest.mark.parametrize("mode", ["direct", "binned"])
+@pytest.mark.parametrize("mode", ["direct", "binned", "table"])
 def test_gradient_vs_oracle(name, mode):
     space, ospace, z, arrays = load_golden(name)
     xs = z["uniform_xs"].astype(np.float64)
     _, gwant = refeval.reference_eval_batch(ospace, xs, [a.astype(np.float64) for a in arrays],
                                             grad=True)
-    ev = _evaluator(space, arrays, grad=True, mode=mode)
+    if mode == "table":
+        ev = _evaluator(space, arrays, grad=True, coeffs="table")
+    else:
+        ev = _evaluator(space, arrays, grad=True, mode=mode)
     out, g, _ = ev(_xs(z, "uniform"))
     g = g.double().cpu().numpy()
     scale = max(1.0, float(np.abs(gwant).max()))

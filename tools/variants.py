@@ -31,6 +31,8 @@ VARIANTS = {
     "binned_b4_ldg_t128": dict(mode="binned", stage="ldg", block=128, unroll_cosets=False, bin=4),
     "binned_b4_sites_t128": dict(mode="binned", stage="tma", block=128, unroll_cosets=False, bin=4, form="sites"),
     "binned_b4_sites_unroll": dict(mode="binned", stage="tma", block=128, unroll_cosets=True, bin=4, form="sites"),
+    "binned_b6_t256_loop_fix": dict(mode="binned", stage="tma", block=256, unroll_cosets=False, bin=6),
+    "binned_b8_table": dict(mode="binned", stage="tma", block=128, unroll_cosets=False, bin=8, coeffs="table"),
 }
 
 
