@@ -80,6 +80,8 @@ typedef struct sg_module_info {
   int32_t bin;                 /* bin edge, in lattice cells */
   int32_t brick[SG_MAX_DIM];   /* brick extent per axis (elements), C order */
   int64_t extents[SG_MAX_DIM]; /* unpadded extents (equal for all cosets in binned mode) */
+  int32_t chunk;               /* binned: queries per CTA work item */
+  int32_t static_smem;         /* informational: static shared memory of the kernel */
 } sg_module_info;
 
 enum { SG_MODE_DIRECT = 0, SG_MODE_BINNED = 1 };

@@ -164,7 +164,7 @@ __device__ __forceinline__ int sg_bin_of(const float* __restrict__ xs, long long
 }
 
 constexpr int SG_SORT_THREADS = 1024;
-constexpr int SG_SMEM_BINS = 24576;     // bins that fit the privatized shared histograms
+constexpr int SG_SMEM_BINS = 4096;      // bins that fit the privatized shared histograms
 constexpr int SG_SCAN_TILE = 8192;      // elements per CTA in the device-wide scan
 
 // K1: per-CTA histogram of a contiguous query range -> mat[bin * G + cta] (no atomics
@@ -269,6 +269,24 @@ __global__ void sg_bin_starts(const int* __restrict__ mat, long long nbins, int 
   long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (b < nbins) starts[b] = mat[b * G];
   if (b == nbins) starts[b] = (int)n;
+}
+
+// work items for the evaluation grid: (bin, first query) per chunk of a bin; -1 = idle CTA
+__global__ void __launch_bounds__(1024) sg_make_items(const int* __restrict__ starts, int nbins,
+                                                      int chunk, int2* __restrict__ items,
+                                                      int max_items) {
+  __shared__ int sh[32];
+  const int per = (nbins + 1023) / 1024;
+  const int lo = threadIdx.x * per, hi = min(nbins, lo + per);
+  int mine = 0;
+  for (int b = lo; b < hi; ++b) mine += (starts[b + 1] - starts[b] + chunk - 1) / chunk;
+  int total;
+  int at = sg_block_excl_scan(mine, sh, &total);
+  for (int b = lo; b < hi; ++b) {
+    const int s0 = starts[b], s1 = starts[b + 1];
+    for (int q = s0; q < s1; q += chunk) items[at++] = make_int2(b, q);
+  }
+  for (int i = total + threadIdx.x; i < max_items; i += 1024) items[i] = make_int2(-1, 0);
 }
 
 // K3: scatter (x, y, z, index) records to their sorted positions
@@ -412,7 +430,7 @@ int sg_module_load(const void* image, size_t image_len, const char* entry, int d
       delete m;
       return fail(SG_EINVAL, "too many bins");
     }
-    if (m->info.smem_bytes > 48 * 1024) {
+    {
       e = cudaFuncSetAttribute((const void*)m->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                m->info.smem_bytes);
       if (e != cudaSuccess) {
@@ -640,11 +658,14 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
                 nb, SG_SMEM_BINS);
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, m->device);
-  const long long G = std::max<long long>(1, std::min<long long>((n + 8191) / 8192, 8LL * dev_sms));
+  const long long G = std::max<long long>(1, std::min<long long>((n + 32767) / 32768, 2LL * dev_sms));
   const long long per = (n + G - 1) / G;
   const long long mlen = (long long)nb * G;
   const long long ntiles = (mlen + SG_SCAN_TILE - 1) / SG_SCAN_TILE;
-  const size_t need = (size_t)n * sizeof(float4) + ((size_t)mlen + ntiles + nb + 1) * sizeof(int) + 512;
+  const int chunk = std::max(32, in.chunk);
+  const long long max_items = (n + chunk - 1) / chunk + (long long)nb;
+  const size_t need = (size_t)n * sizeof(float4) + ((size_t)mlen + ntiles + nb + 1) * sizeof(int) +
+                      (size_t)max_items * sizeof(int2) + 1024;
   if (m->bin_scratch_bytes < need) {
     if (m->bin_scratch) cudaFree(m->bin_scratch);
     m->bin_scratch = nullptr;
@@ -656,6 +677,7 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
   int* mat = (int*)(sorted + n);
   int* tile_sums = mat + mlen;
   int* starts = tile_sums + ntiles;
+  int2* items = (int2*)(((uintptr_t)(starts + nb + 1) + 15) & ~(uintptr_t)15);
   BinGeom g{};
   g.dim = in.dim;
   g.bin = in.bin;
@@ -682,6 +704,7 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
   sg_bin_starts<<<(unsigned)((nb + 256) / 256), 256, 0, st>>>(mat, (long long)nb, (int)G, (long long)n,
                                                               starts);
   CU(cudaGetLastError());
+  sg_make_items<<<1, 1024, 0, st>>>(starts, (int)nb, chunk, items, (int)max_items);
   sg_bin_scatter<<<(unsigned)G, SG_SORT_THREADS, 2 * nb * sizeof(int), st>>>(
       (const float*)xs, (long long)n, per, g, mat, sorted);
   CU(cudaGetLastError());
@@ -715,9 +738,10 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
   unsigned* err = m->d_err;
   const void* sp = sorted;
   const void* stp = starts;
-  void* args[] = {(void*)&sp, (void*)&stp, (void*)&out, (void*)&grad, (void*)&dbg, (void*)&err,
-                  (void*)&cs, (void*)&tm};
-  CU(cudaLaunchKernel((const void*)m->kernel, dim3((unsigned)nb), dim3(in.block), args,
+  const void* itp = items;
+  void* args[] = {(void*)&sp, (void*)&stp, (void*)&itp, (void*)&out, (void*)&grad, (void*)&dbg,
+                  (void*)&err, (void*)&cs, (void*)&tm};
+  CU(cudaLaunchKernel((const void*)m->kernel, dim3((unsigned)max_items), dim3(in.block), args,
                       (size_t)in.smem_bytes, st));
   return SG_OK;
 }

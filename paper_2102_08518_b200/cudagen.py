@@ -60,7 +60,9 @@ class GenConfig:
     dbg: bool = False
     min_blocks: int = 0          # __launch_bounds__ second argument (0 = let ptxas pick)
     mode: str = "direct"         # "direct": gathers through L1/L2; "binned": bin + smem bricks
-    bin: int = 8                 # binned: bin edge in lattice cells
+    bin: int = 0                 # binned: bin edge in lattice cells (multiple of 4; 0 = auto)
+    chunk: int = 4096            # binned: queries per CTA work item (a bin is split in chunks)
+    brick_budget: int = 112 * 1024   # binned auto-bin: shared-memory budget for the bricks
     stage: str = "tma"           # binned: brick staging, "tma" (cp.async.bulk.tensor) | "ldg"
 
     def __post_init__(self):
@@ -292,6 +294,7 @@ class CudaProgram:
     bin: int = 0
     brick: tuple = ()
     smem_bytes: int = 0
+    chunk: int = 0
     stage_tma: bool = False
     rounding: int = 1
     meta: dict = field(default_factory=dict)
@@ -385,12 +388,19 @@ def generate(space, config: GenConfig | None = None, extents=None,
         margin = h + 2   # f32 binning may be off by one cell; rounding/cosets add one more
         H = margin
         unit = 4  # TMA: innermost box extent x 4 B must be a multiple of 16 B
+        if bin_ == 0:   # largest multiple of 4 whose bricks (all cosets) fit the budget
+            bin_ = 4
+            while M * 4 * (-(-(bin_ + 4 + 2 * margin) // unit) * unit) ** s <= cfg.brick_budget \
+                    and bin_ + 4 <= max(ext[0]):
+                bin_ += 4
+        if bin_ % 4:
+            raise ValueError("bin must be a multiple of 4 (TMA box coordinates must be 16-B aligned)")
         nb = [-(-e // bin_) for e in ext[0]]
-        while int(np.prod(nb)) > 24576:        # the binning kernels' shared histogram limit
-            bin_ += 2
+        while int(np.prod(nb)) > 4096:         # the binning kernels' shared histogram limit
+            bin_ += 4
             nb = [-(-e // bin_) for e in ext[0]]
-        # TMA boxes: every extent a multiple of 4 elements (measured: boxes with 13/14-wide
-        # outer dims fault on sm_100a), padded global extents multiples of 16
+        # TMA boxes: every extent a multiple of 4 elements and start coordinates multiples
+        # of 4 (measured on sm_100a: other alignments fault), padded extents multiples of 16
         brick = [-(-(bin_ + 2 * margin) // unit) * unit] * s
         prow = [max(ext[0][d] + 2 * H, (nb[d] - 1) * bin_ + brick[d]) for d in range(s)]
         prow = [-(-v // 16) * 16 for v in prow]
@@ -451,7 +461,8 @@ def generate(space, config: GenConfig | None = None, extents=None,
     # ---- tables ------------------------------------------------------------
     smem = []     # (name, ctype, values)
     use_sigma = t.nsub > 1 and len(space.planes) > 0 and len(set(t.sigma)) > 1
-    if use_sigma:
+    sigma_global = use_sigma and len(t.sigma) > 4096
+    if use_sigma and not sigma_global:
         smem.append(("sg_sigma", "int", list(t.sigma)))
     if not t.uniform_T:
         smem.append(("sg_T", T, [float(v) for tr in t.transforms for row in tr for v in row]))
@@ -522,6 +533,9 @@ def generate(space, config: GenConfig | None = None, extents=None,
             lit = ", ".join(dlit(Fraction(v)) for v in vals)
         A(f"__constant__ {ctype} {name}_c[{len(vals)}] = {{{lit}}};")
 
+    if sigma_global:
+        A(f"__device__ const int sg_sigma_g[{len(t.sigma)}] = {{{', '.join(str(v) for v in t.sigma)}}};")
+
     # ---- kernel -------------------------------------------------------------
     lb = f"{cfg.block}, {cfg.min_blocks}" if cfg.min_blocks else f"{cfg.block}"
     body = []
@@ -544,14 +558,17 @@ def generate(space, config: GenConfig | None = None, extents=None,
     else:
         B(f'extern "C" __global__ void __launch_bounds__({lb}) {ENTRY}(')
         B("    const float4* __restrict__ sorted, const int* __restrict__ starts,")
+        B("    const int2* __restrict__ items,")
         B(f"    {T}* __restrict__ out, {T}* __restrict__ grad, int* __restrict__ dbg,")
         B("    unsigned* __restrict__ err, SgCosets vol, const __grid_constant__ SgTmaps tm) {")
         B("  extern __shared__ __align__(128) float sg_brick[];")
         B("  __shared__ __align__(8) unsigned long long sg_bar;")
         for name, ctype, vals in smem:
             B(f"  __shared__ __align__(16) {ctype} {name}[{len(vals)}];")
-        # bin coordinates (row-major over nb)
-        B("  const int bin = blockIdx.x;")
+        # work item of this CTA: (bin, first sorted query); bin < 0 -> no work
+        B("  const int2 item = items[blockIdx.x];")
+        B("  if (item.x < 0) return;")
+        B("  const int bin = item.x;")
         rem = "bin"
         for d in range(s - 1, -1, -1):
             if d == 0:
@@ -603,8 +620,8 @@ def generate(space, config: GenConfig | None = None, extents=None,
         B("  __syncthreads();")
         if cfg.stage == "tma":
             B('  asm volatile("{\\n .reg .pred p;\\n SG_WAIT_%=:\\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\\n @!p bra SG_WAIT_%=;\\n}" :: "r"(sg_bar_a) : "memory");')
-        B("  const int q_end = starts[bin + 1];")
-        B(f"  for (int qq = starts[bin] + threadIdx.x; qq < q_end; qq += {cfg.block}) {{")
+        B(f"  const int q_end = min(starts[bin + 1], item.y + {cfg.chunk});")
+        B(f"  for (int qq = item.y + threadIdx.x; qq < q_end; qq += {cfg.block}) {{")
         B("  const float4 q4 = sorted[qq];")
         B("  const long long qi = (long long)__float_as_int(q4.w);")
         comps = ["x", "y", "z"]
@@ -708,7 +725,9 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 L(f"q |= (({acc or '0.0'}) >= {dlit(off)}) ? {1 << i}u : 0u;")
             if t.compress:
                 L(f"q = q % {P}u;")
-            if use_sigma:
+            if sigma_global:
+                L("int sub = __ldg(&sg_sigma_g[q]);")
+            elif use_sigma:
                 L("int sub = sg_sigma[q];")
             else:
                 v = t.sigma[0] if t.sigma else 0
@@ -1013,6 +1032,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
         has_dbg=cfg.dbg, config=cfg, space=space,
         mode=cfg.mode, bin=bin_ if binned else 0, brick=tuple(brick) if binned else (),
         smem_bytes=smem_bytes if binned else 0, stage_tma=binned and cfg.stage == "tma",
+        chunk=cfg.chunk if binned else 0,
         rounding=(0 if (rm0.shape == PARALLELEPIPED and rm0.rounding == "floor") else 1),
         meta={"fetch_mode": fetch_mode, "K": t.K, "nsub": t.nsub, "n": t.n, "reach": h,
               "smem_tables": [x[0] for x in smem], "lut_entries": len(lut)})

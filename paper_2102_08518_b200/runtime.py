@@ -47,7 +47,8 @@ class sg_module_info(ctypes.Structure):
                 ("mode", ctypes.c_int32), ("rounding", ctypes.c_int32),
                 ("stage_tma", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
                 ("bin", ctypes.c_int32), ("brick", ctypes.c_int32 * SG_MAX_DIM),
-                ("extents", ctypes.c_int64 * SG_MAX_DIM)]
+                ("extents", ctypes.c_int64 * SG_MAX_DIM), ("chunk", ctypes.c_int32),
+                ("static_smem", ctypes.c_int32)]
 
 
 _lib = None
@@ -186,6 +187,7 @@ class Module:
         info.stage_tma = int(prog.stage_tma)
         info.smem_bytes = prog.smem_bytes
         info.bin = prog.bin
+        info.chunk = prog.chunk
         for d, e in enumerate(prog.brick):
             info.brick[d] = e
         for d, e in enumerate(prog.extents[0]):

@@ -4,7 +4,7 @@ mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" 2>&1 | tail -2
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -8
 timeout 600 python tools/variants.py ${1:-c2} 2>&1 | grep -E "Grecon|FAIL|Error" 
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_variants.csv python tools/variants.py ${1:-c2} --only binned_b4_t128_loop --reps 2 > /dev/null 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_variants.csv python tools/variants.py ${1:-c2} --only binned_auto_t256 --reps 2 > /dev/null 2>&1
 python - <<'PY'
 import csv
 lines=open("gpurun_out/launches_variants.csv").read().splitlines()

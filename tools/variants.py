@@ -22,17 +22,17 @@ from paper_2102_08518_b200 import runtime  # noqa: E402
 
 VARIANTS = {
     "direct": dict(mode="direct", block=128),
-    "binned_b8_t256_loop": dict(mode="binned", stage="tma", block=256, unroll_cosets=False, bin=8),
-    "binned_b8_t256_unroll": dict(mode="binned", stage="tma", block=256, unroll_cosets=True, bin=8),
-    "binned_b6_t256_loop": dict(mode="binned", stage="tma", block=256, unroll_cosets=False, bin=6),
-    "binned_b4_t128_loop": dict(mode="binned", stage="tma", block=128, unroll_cosets=False, bin=4),
-    "binned_b4_t128_unroll": dict(mode="binned", stage="tma", block=128, unroll_cosets=True, bin=4),
-    "binned_b4_t256_loop": dict(mode="binned", stage="tma", block=256, unroll_cosets=False, bin=4),
-    "binned_b4_ldg_t128": dict(mode="binned", stage="ldg", block=128, unroll_cosets=False, bin=4),
-    "binned_b4_sites_t128": dict(mode="binned", stage="tma", block=128, unroll_cosets=False, bin=4, form="sites"),
-    "binned_b4_sites_unroll": dict(mode="binned", stage="tma", block=128, unroll_cosets=True, bin=4, form="sites"),
-    "binned_b6_t256_loop_fix": dict(mode="binned", stage="tma", block=256, unroll_cosets=False, bin=6),
-    "binned_b8_table": dict(mode="binned", stage="tma", block=128, unroll_cosets=False, bin=8, coeffs="table"),
+    "binned_auto_t256": dict(mode="binned", block=256, unroll_cosets=False),
+    "binned_auto_t256_unroll": dict(mode="binned", block=256, unroll_cosets=True),
+    "binned_auto_t512": dict(mode="binned", block=512, unroll_cosets=False),
+    "binned_auto_t256_c2048": dict(mode="binned", block=256, unroll_cosets=False, chunk=2048),
+    "binned_auto_t256_c8192": dict(mode="binned", block=256, unroll_cosets=False, chunk=8192),
+    "binned_b8_t256": dict(mode="binned", block=256, unroll_cosets=False, bin=8),
+    "binned_b12_t256": dict(mode="binned", block=256, unroll_cosets=False, bin=12),
+    "binned_auto_ldg": dict(mode="binned", block=256, unroll_cosets=False, stage="ldg"),
+    "binned_auto_sites": dict(mode="binned", block=256, unroll_cosets=False, form="sites"),
+    "binned_auto_sites_unroll": dict(mode="binned", block=256, unroll_cosets=True, form="sites"),
+    "binned_auto_table": dict(mode="binned", block=256, unroll_cosets=False, coeffs="table"),
 }
 
 
