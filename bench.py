@@ -36,12 +36,23 @@ sys.path.insert(0, str(ROOT))
 
 PROFILES = ROOT / "profiles"
 
-# name -> (space fixture, extents per coset, queries per GPU, query kind, grad)
+# name -> workload (BASELINE.json configs, restated concretely in SURVEY.md 8d)
 CONFIGS = {
     "c1": dict(space="tricubic", extents=(64, 64, 64), queries=1 << 20, kind="uniform",
-               grad=False, desc="tensor-product tricubic B-spline on Z^3, 64^3, 2^20 uniform"),
+               grad=False, scaling="weak",
+               desc="tensor-product tricubic B-spline on Z^3, 64^3, 2^20 uniform"),
     "c2": dict(space="bcc_box5", extents=(101, 101, 101), queries=1 << 24, kind="uniform",
-               grad=False, desc="BCC quintic box spline (4 dirs x2), 2x101^3 coset-split, 2^24 uniform"),
+               grad=False, scaling="weak",
+               desc="BCC quintic box spline (4 dirs x2), 2x101^3 coset-split, 2^24 uniform"),
+    "c3": dict(space="bcc_voronoi2", extents=(203, 203, 203), queries=1 << 26, kind="rays",
+               rays=(512, 512, 256), grad=False, scaling="weak",
+               desc="BCC Voronoi spline (order 2, piecewise cubic), 2x203^3, 2^26 ray-ordered"),
+    "c4": dict(space="fcc_box6", extents=(161, 161, 161), queries=1 << 26, kind="uniform",
+               grad=True, scaling="weak",
+               desc="FCC 6-direction box spline, 4x161^3, 2^26 uniform, value + gradient"),
+    "c5": dict(space="bcc_voronoi2", extents=(406, 406, 406), queries=1 << 30, kind="rays",
+               rays=(1024, 1024, 1024), grad=False, scaling="strong",
+               desc="BCC Voronoi spline (order 2), 2x406^3, 2^30 ray-ordered sharded over the GPUs"),
 }
 DEFAULT_CONFIG = "c2"
 
@@ -56,10 +67,12 @@ def default_config_name():
 
 
 def gen_config_for(space, grad=False, **over):
+    """The tuned default variant per space (see profiles/ for the variant sweeps)."""
     from paper_2102_08518_b200 import GenConfig, ScheduleParams
     n = space.stencil_size
     kw = dict(params=ScheduleParams(1, n, "predicated"), float_width="f32",
-              unroll_cosets=space.ncosets == 1, form="horner", block=128, grad=grad)
+              unroll_cosets=space.ncosets == 1, form="horner", block=256, grad=grad,
+              mode="binned", coeffs="table" if space.nref > 2 else "imm")
     kw.update(over)
     return GenConfig(**kw)
 
@@ -173,7 +186,7 @@ def _cpu_worker(i):
     return time.perf_counter() - t0
 
 
-def cpu_baseline(space_name, arrays_f32, xs_f32, budget_s=15.0, shard=1 << 14):
+def cpu_baseline(space_name, arrays_f32, xs_f32, budget_s=15.0, shard=1 << 14, pool=None):
     """Time the oracle port (restatement of reference_eval_batch, numpy f64) on all
     host cores over a bounded sample of the same workload."""
     import multiprocessing as mp
@@ -181,40 +194,65 @@ def cpu_baseline(space_name, arrays_f32, xs_f32, budget_s=15.0, shard=1 << 14):
     path = str(SPACES_DIR / f"{space_name}.json")
     for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ[k] = "1"
-    _CPU_STATE.update(path=path, arrays=[a.astype(np.float64) for a in arrays_f32],
-                      xs=xs_f32, shard=shard)
+    if _CPU_STATE.get("path") != path or _CPU_STATE.get("xs") is not xs_f32:
+        _CPU_STATE.update(path=path, arrays=[a.astype(np.float64) for a in arrays_f32],
+                          xs=xs_f32, shard=shard, rate1=None)
     cores = len(os.sched_getaffinity(0))
-    t1 = _cpu_worker(0)     # calibrate on one shard
-    rate1 = shard / t1
+    if _CPU_STATE.get("rate1") is None:
+        t1 = _cpu_worker(0)     # calibrate on one shard
+        _CPU_STATE["rate1"] = shard / t1
+    rate1 = _CPU_STATE["rate1"]
     nshards = max(cores, int(budget_s * rate1 * cores / shard) // cores * cores)
     nshards = min(nshards, max(1, len(xs_f32) // shard))
-    ctx = mp.get_context("fork")
+    own = pool is None
+    if own:
+        pool = mp.get_context("fork").Pool(cores)
     t0 = time.perf_counter()
-    with ctx.Pool(cores) as pool:
-        pool.map(_cpu_worker, range(nshards))
+    pool.map(_cpu_worker, range(nshards), chunksize=1)
     wall = time.perf_counter() - t0
+    if own:
+        pool.close()
+        pool.join()
     n = nshards * shard
     return {"value": n / wall / 1e9, "unit": "Grecon/s", "cores": cores, "kind": "port",
             "sample": f"{n} of the configuration's queries ({nshards} shards of {shard}), "
-                      f"oracle/refeval.reference_eval_batch (numpy f64) on {cores} processes, "
-                      f"{wall:.1f}s; 1-core rate {rate1:.3e} q/s"}
+                      f"oracle/refeval.reference_eval_batch (numpy f64, restatement of "
+                      f"splinegen.oracle.reference_eval_batch) on {cores} processes, "
+                      f"{wall:.2f}s; 1-core rate {rate1:.3e} q/s"}
 
 
 # -- workload ---------------------------------------------------------------------------
 
 
-def make_inputs(cfg_name, rank, device):
-    import torch
+def query_range(cfg_name, rank, world):
+    """This rank's slice of the global query stream (weak: n per rank; strong: shard)."""
+    from paper_2102_08518_b200.dist import shard_range
+    c = CONFIGS[cfg_name]
+    if c["scaling"] == "strong":
+        return shard_range(c["queries"], rank, world)
+    return rank * c["queries"], (rank + 1) * c["queries"]
+
+
+def make_queries(cfg_name, lo, hi, device):
+    from paper_2102_08518_b200 import queries
+    c = CONFIGS[cfg_name]
+    if c["kind"] == "rays":
+        w, h, st = c["rays"]
+        total = w * h * st
+        # weak-scaled ranks beyond the first replay the ray stream (same work per rank)
+        return queries.rays(lo % total, lo % total + (hi - lo), c["extents"], w, h, st, 2, device)
+    return queries.uniform(lo, hi, c["extents"], 1, device)
+
+
+def make_inputs(cfg_name, rank, device, world=1):
     from paper_2102_08518_b200 import load_fixture
     c = CONFIGS[cfg_name]
     space = load_fixture(c["space"])
     ext = c["extents"]
     rng = np.random.default_rng(0)  # make_volume(seed=0): U[0,1), cosets in order
     arrays = [rng.random(ext).astype(np.float32) for _ in range(space.ncosets)]
-    g = torch.Generator(device=device)
-    g.manual_seed(1 + rank)
-    spans = torch.tensor(ext, dtype=torch.float32, device=device)
-    xs = torch.rand((c["queries"], space.dim), generator=g, device=device) * spans
+    lo, hi = query_range(cfg_name, rank, world)
+    xs = make_queries(cfg_name, lo, hi, device)
     return space, arrays, xs
 
 
@@ -225,7 +263,7 @@ def run_ours(args, rank, world, device):
     from paper_2102_08518_b200 import runtime
 
     c = CONFIGS[args.config]
-    space, arrays, xs = make_inputs(args.config, rank, device)
+    space, arrays, xs = make_inputs(args.config, rank, device, world)
     _, prog = build_program(args.config)
     # volume: rank 0's synthetic data broadcast over NCCL (replicated per GPU)
     if world > 1:
@@ -237,13 +275,14 @@ def run_ours(args, rank, world, device):
         ev = Evaluator(space, arrays, prog=prog, device=device.index)
     n = xs.shape[0]
     out = torch.empty(n, dtype=torch.float32, device=device)
+    grad = torch.empty((n, space.dim), dtype=torch.float32, device=device) if prog.has_grad else None
     stream = torch.cuda.current_stream(device)
     l2_flush = None
     if n * space.dim * 4 < 2 * 126e6:
         l2_flush = torch.empty(int(256e6) // 4, dtype=torch.float32, device=device)
 
     def step():
-        runtime.eval_device(ev.module, ev.volume, xs, out, stream=stream)
+        runtime.eval_device(ev.module, ev.volume, xs, out, grad, stream=stream)
 
     for _ in range(args.warmup):
         step()
@@ -273,13 +312,15 @@ def run_ours(args, rank, world, device):
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     ms = float(tt.item())
-    total_q = n * world * args.steps
+    per_step_total = c["queries"] if c["scaling"] == "strong" else n * world
+    total_q = per_step_total * args.steps
     value = total_q / (ms / 1e3) / 1e9
     kernel_ms = ms / args.steps
 
     # ---- end to end through the C-ABI host path (pinned buffers)
     xs_host = xs.cpu().pin_memory()
     out_host = torch.empty(n, dtype=torch.float32).pin_memory()
+    grad_host = torch.empty((n, space.dim), dtype=torch.float32).pin_memory() if grad is not None else None
     e2e_steps = max(3, min(args.steps, 20))
     lib = runtime.lib()
 
@@ -287,7 +328,8 @@ def run_ours(args, rank, world, device):
         runtime._check(lib.sg_eval_host(ev.module.handle, ev.volume.handle,
                                         runtime.ctypes.c_void_p(xs_host.data_ptr()), n,
                                         runtime.ctypes.c_void_p(out_host.data_ptr()),
-                                        runtime.ctypes.c_void_p(0), 1 << 21))
+                                        runtime.ctypes.c_void_p(grad_host.data_ptr() if grad_host is not None else 0),
+                                        1 << 22))
     host_step()
     if world > 1:
         dist.barrier()
@@ -298,7 +340,7 @@ def run_ours(args, rank, world, device):
     te = torch.tensor([e2e_s], dtype=torch.float64, device=device)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = n * world * e2e_steps / float(te.item()) / 1e9
+    e2e_value = per_step_total * e2e_steps / float(te.item()) / 1e9
     # correctness spot check of the timed kernel against the host path
     ref_out = out[:4096].cpu()
     assert torch.equal(ref_out, out_host[:4096]), "device and host paths disagree"
@@ -324,7 +366,7 @@ def run_ours(args, rank, world, device):
         "metric": "G reconstructions/sec per B200 (fraction of FP32 roofline in roofline)",
         "value": round(value, 4), "unit": "Grecon/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(kernel_ms, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": c["scaling"], "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": args.config + ": " + c["desc"], "space": c["space"],
                    "extents": list(c["extents"]), "cosets": space.ncosets,
                    "queries_per_gpu": n, "query_kind": c["kind"],
@@ -332,8 +374,10 @@ def run_ours(args, rank, world, device):
                    "l2": "L2 flushed between steps" if l2_flush is not None
                    else "query stream > L2 (126 MB); volume L2-resident by design"},
         "e2e": {"value": round(e2e_value, 4), "unit": "Grecon/s",
-                "h2d_bytes_per_step": n * space.dim * 4, "d2h_bytes_per_step": n * 4,
-                "steps": e2e_steps},
+                "h2d_bytes_per_step": n * space.dim * 4,
+                "d2h_bytes_per_step": n * 4 * (1 + (space.dim if grad is not None else 0)),
+                "steps": e2e_steps, "path": "sg_eval_host (C ABI, pinned host buffers, "
+                "H2D / kernel / D2H pipelined over 2^22-query chunks)"},
         "gpu_launches": args.steps,
         "roofline": roof,
         "clocks": clk.summary(),
@@ -342,38 +386,56 @@ def run_ours(args, rank, world, device):
     }
     if not args.no_cpu:
         xs_np = xs[: 1 << 20].cpu().numpy()
-        line["cpu_baseline"] = cpu_baseline(c["space"], arrays, xs_np, budget_s=args.cpu_budget)
+        line["cpu_baseline"] = cpu_baseline(c["space"], arrays, xs_np, budget_s=args.cpu_budget,
+                                            shard=1 << 12)
     return line
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU evaluator (oracle port) on all host cores."""
+    """--impl reference: the reference's CPU evaluator (oracle port) on all host cores,
+    each step a bounded sample of the configuration's query stream."""
     if rank != 0:
         return None
+    import multiprocessing as mp
     from paper_2102_08518_b200 import load_fixture
     c = CONFIGS[args.config]
     space = load_fixture(c["space"])
     rng = np.random.default_rng(0)
     arrays = [rng.random(c["extents"]).astype(np.float32) for _ in range(space.ncosets)]
-    xs = (np.random.default_rng(1).random((1 << 20, space.dim)) *
-          np.array(c["extents"])).astype(np.float32)
-    per_step = max(5.0, 60.0 / max(1, args.steps + args.warmup))
+    xs = make_queries(args.config, 0, 1 << 18, "cpu").numpy()
+    total_budget = 150.0                       # seconds for the whole --steps/--warmup run
+    per_step = total_budget / (args.steps + args.warmup)
+    cores = len(os.sched_getaffinity(0))
+    shard = 1 << 11
+    _cpu_worker_init(args.config, arrays, xs, shard)
+    pool = mp.get_context("fork").Pool(cores)
     vals = []
-    for i in range(args.warmup + args.steps):
-        r = cpu_baseline(c["space"], arrays, xs, budget_s=per_step)
-        if i >= args.warmup:
-            vals.append(r)
+    try:
+        for i in range(args.warmup + args.steps):
+            r = cpu_baseline(c["space"], arrays, xs, budget_s=per_step, shard=shard, pool=pool)
+            if i >= args.warmup:
+                vals.append(r)
+    finally:
+        pool.close()
+        pool.join()
     v = statistics.median([r["value"] for r in vals])
     return {
-        "impl": "reference", "metric": "G reconstructions/sec per B200 (fraction of FP32 roofline in roofline)",
+        "impl": "reference",
+        "metric": "G reconstructions/sec per B200 (fraction of FP32 roofline in roofline)",
         "value": v, "unit": "Grecon/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
+        "ms_per_step": None, "higher_is_better": True, "scaling": c["scaling"], "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config + ": " + c["desc"], "space": c["space"],
-                   "extents": list(c["extents"])},
+                   "extents": list(c["extents"]), "query_kind": c["kind"]},
         "cpu_baseline": {**vals[-1], "value": v},
         "e2e": {"value": v, "unit": "Grecon/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+
+
+def _cpu_worker_init(cfg_name, arrays, xs, shard):
+    from paper_2102_08518_b200.model import SPACES_DIR
+    _CPU_STATE.update(path=str(SPACES_DIR / f"{CONFIGS[cfg_name]['space']}.json"),
+                      arrays=[a.astype(np.float64) for a in arrays], xs=xs, shard=shard, rate1=None)
 
 
 def main():
