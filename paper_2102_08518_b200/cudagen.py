@@ -895,13 +895,15 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 if parts:
                     L(f"gacc{e} += {' + '.join(parts)};")
 
-        def nested_horner(coef, u):
-            """sum_e coef(e) u^e over tab['exps'] by nested Horner (axis 0 outermost).
-            coef(e) returns an operand string or None (absent)."""
+        def nested_horner(coef, u, exps=None):
+            """sum_e coef(e) u^e over the exponent set (default tab['exps']) by nested
+            Horner (axis 0 outermost).  coef(e) returns an operand string or None."""
+            exps = tab["exps"] if exps is None else exps
+
             def rec(fixed, axis):
                 if axis == s:
                     return coef(tuple(fixed))
-                pows = sorted({e[axis] for e in tab["exps"] if tuple(e[:axis]) == tuple(fixed)})
+                pows = sorted({e[axis] for e in exps if tuple(e[:axis]) == tuple(fixed)})
                 if not pows:
                     return None
                 r = None
@@ -960,7 +962,9 @@ def generate(space, config: GenConfig | None = None, extents=None,
                             return None
                         f = e[a] + 1
                         return f"g{midx[e2]}" if f == 1 else f"{flit(f, fw)} * g{midx[e2]}"
-                    du.append(nested_horner(dcoef, u))
+                    dexps = sorted({tuple(v - (k == a) for k, v in enumerate(e))
+                                    for e in tab["exps"] if e[a] > 0})
+                    du.append(nested_horner(dcoef, u, dexps) if dexps else f"({T})0")
                 add_grad(du, True)
 
         if cfg.coeffs == "table":

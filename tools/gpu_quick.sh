@@ -15,3 +15,5 @@ ki=hdr.index("Kernel Name"); vi=hdr.index("Metric Value")
 for r in rows[1:][-12:]:
     print(f"{r[ki][:40]:40s} {r[vi]}")
 PY
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:sg_eval_kernel -s 2 -c 1 -o gpurun_out/prof_binned -f python tools/variants.py ${1:-c2} --only binned_auto_t256_unroll --reps 2 > /dev/null 2>&1
+ls -la gpurun_out/prof_binned.ncu-rep
