@@ -167,6 +167,58 @@ constexpr int SG_SORT_THREADS = 1024;
 constexpr int SG_SMEM_BINS = 4096;      // bins that fit the privatized shared histograms
 constexpr int SG_SCAN_TILE = 8192;      // elements per CTA in the device-wide scan
 
+__device__ __forceinline__ int sg_bin_xyz(float x, float y, float z, const BinGeom& g) {
+  const float c[3] = {x, y, z};
+  int lin = 0;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    if (d < g.dim) {
+      float xw = c[d] - g.ext[d] * floorf(c[d] * g.inv_ext[d]);
+      int b = (int)floorf(xw * g.inv_bin);
+      b = min(max(b, 0), g.nb[d] - 1);
+      lin = lin * g.nb[d] + b;
+    }
+  }
+  return lin;
+}
+
+// warp-aggregated shared-memory atomic: lanes with the same bin share one atomicAdd
+__device__ __forceinline__ int sg_agg_add(int* counters, int b) {
+  const unsigned act = __activemask();
+  const unsigned peers = __match_any_sync(act, b);
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(peers) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(&counters[b], __popc(peers));
+  base = __shfl_sync(peers, base, leader);
+  return base + __popc(peers & ((1u << lane) - 1));
+}
+
+// Queries of a CTA range are read as float4 triples (4 queries of 3 floats) when the
+// range is 16-B aligned; `visit(i, x, y, z)` is called for every query.
+template <typename F>
+__device__ __forceinline__ void sg_for_queries(const float* __restrict__ xs, long long lo,
+                                               long long hi, const BinGeom& g, F visit) {
+  if (g.dim == 3 && ((lo & 3) == 0) && ((((uintptr_t)xs) & 15) == 0)) {
+    const float4* X4 = reinterpret_cast<const float4*>(xs);
+    const long long g0 = lo >> 2, g1 = hi >> 2;   // full groups
+    for (long long q = g0 + threadIdx.x; q < g1; q += blockDim.x) {
+      const float4 a = X4[3 * q], b = X4[3 * q + 1], c = X4[3 * q + 2];
+      const long long i = q << 2;
+      visit(i, a.x, a.y, a.z);
+      visit(i + 1, a.w, b.x, b.y);
+      visit(i + 2, b.z, b.w, c.x);
+      visit(i + 3, c.y, c.z, c.w);
+    }
+    for (long long i = (g1 << 2) + threadIdx.x; i < hi; i += blockDim.x)
+      visit(i, xs[i * 3], xs[i * 3 + 1], xs[i * 3 + 2]);
+  } else {
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x)
+      visit(i, xs[i * g.dim], g.dim > 1 ? xs[i * g.dim + 1] : 0.f,
+            g.dim > 2 ? xs[i * g.dim + 2] : 0.f);
+  }
+}
+
 // K1: per-CTA histogram of a contiguous query range -> mat[bin * G + cta] (no atomics
 // on global memory; the (bin, cta) matrix is scanned bin-major next).
 __global__ void __launch_bounds__(SG_SORT_THREADS) sg_bin_count(
@@ -178,8 +230,9 @@ __global__ void __launch_bounds__(SG_SORT_THREADS) sg_bin_count(
   __syncthreads();
   const long long lo = (long long)blockIdx.x * per;
   const long long hi = min(n, lo + per);
-  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x)
-    atomicAdd(&hist[sg_bin_of(xs, i, g)], 1);
+  sg_for_queries(xs, lo, hi, g, [&](long long, float x, float y, float z) {
+    sg_agg_add(hist, sg_bin_xyz(x, y, z, g));
+  });
   __syncthreads();
   for (int b = threadIdx.x; b < g.nbins; b += blockDim.x) mat[(long long)b * G + blockIdx.x] = hist[b];
 }
@@ -294,26 +347,16 @@ __global__ void __launch_bounds__(SG_SORT_THREADS) sg_bin_scatter(
     const float* __restrict__ xs, long long n, long long per, BinGeom g,
     const int* __restrict__ mat, float4* __restrict__ sorted) {
   extern __shared__ int sh[];
-  int* base = sh;
-  int* cnt = sh + g.nbins;
+  int* cnt = sh;   // running position per bin, seeded with this CTA's global offsets
   const int G = gridDim.x;
-  for (int b = threadIdx.x; b < g.nbins; b += blockDim.x) {
-    base[b] = mat[(long long)b * G + blockIdx.x];
-    cnt[b] = 0;
-  }
+  for (int b = threadIdx.x; b < g.nbins; b += blockDim.x) cnt[b] = mat[(long long)b * G + blockIdx.x];
   __syncthreads();
   const long long lo = (long long)blockIdx.x * per;
   const long long hi = min(n, lo + per);
-  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-    int b = sg_bin_of(xs, i, g);
-    int pos = base[b] + atomicAdd(&cnt[b], 1);
-    float4 r;
-    r.x = xs[i * g.dim];
-    r.y = g.dim > 1 ? xs[i * g.dim + 1] : 0.f;
-    r.z = g.dim > 2 ? xs[i * g.dim + 2] : 0.f;
-    r.w = __int_as_float((int)i);
-    sorted[pos] = r;
-  }
+  sg_for_queries(xs, lo, hi, g, [&](long long i, float x, float y, float z) {
+    const int pos = sg_agg_add(cnt, sg_bin_xyz(x, y, z, g));
+    sorted[pos] = make_float4(x, y, z, __int_as_float((int)i));
+  });
 }
 
 extern "C" {
@@ -659,7 +702,7 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, m->device);
   const long long G = std::max<long long>(1, std::min<long long>((n + 32767) / 32768, 2LL * dev_sms));
-  const long long per = (n + G - 1) / G;
+  const long long per = ((n + G - 1) / G + 3) & ~3LL;   // multiple of 4: float4 query groups
   const long long mlen = (long long)nb * G;
   const long long ntiles = (mlen + SG_SCAN_TILE - 1) / SG_SCAN_TILE;
   const int chunk = std::max(32, in.chunk);
@@ -705,7 +748,7 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
                                                               starts);
   CU(cudaGetLastError());
   sg_make_items<<<1, 1024, 0, st>>>(starts, (int)nb, chunk, items, (int)max_items);
-  sg_bin_scatter<<<(unsigned)G, SG_SORT_THREADS, 2 * nb * sizeof(int), st>>>(
+  sg_bin_scatter<<<(unsigned)G, SG_SORT_THREADS, nb * sizeof(int), st>>>(
       (const float*)xs, (long long)n, per, g, mat, sorted);
   CU(cudaGetLastError());
   SgCosets cs{};

@@ -464,10 +464,16 @@ def generate(space, config: GenConfig | None = None, extents=None,
     sigma_global = use_sigma and len(t.sigma) > 4096
     if use_sigma and not sigma_global:
         smem.append(("sg_sigma", "int", list(t.sigma)))
-    if not t.uniform_T:
-        smem.append(("sg_T", T, [float(v) for tr in t.transforms for row in tr for v in row]))
-    if not t.uniform_tp:
-        smem.append(("sg_tp", T, [float(v) for tp in t.tshift for v in tp]))
+    tq = s == 3 and fw == F32 and not (t.uniform_T and t.uniform_tp)
+    if tq:
+        # rows (T[d][0], T[d][1], T[d][2], t'[d]) per sub-region: 3 LDS.128 per coset
+        smem.append(("sg_Tq", T, [float(v) for tr, tp in zip(t.transforms, t.tshift)
+                                  for d in range(3) for v in (*tr[d], tp[d])]))
+    else:
+        if not t.uniform_T:
+            smem.append(("sg_T", T, [float(v) for tr in t.transforms for row in tr for v in row]))
+        if not t.uniform_tp:
+            smem.append(("sg_tp", T, [float(v) for tp in t.tshift for v in tp]))
     fetch_mode = "uniform" if t.uniform_stencil else ("affine" if t.affine is not None else "table")
     if fetch_mode != "uniform" and not same_geom and not cfg.unroll_cosets:
         pass  # per-coset strides are compile-time constants in unrolled mode only; handled below
@@ -621,8 +627,11 @@ def generate(space, config: GenConfig | None = None, extents=None,
         if cfg.stage == "tma":
             B('  asm volatile("{\\n .reg .pred p;\\n SG_WAIT_%=:\\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\\n @!p bra SG_WAIT_%=;\\n}" :: "r"(sg_bar_a) : "memory");')
         B(f"  const int q_end = min(starts[bin + 1], item.y + {cfg.chunk});")
-        B(f"  for (int qq = item.y + threadIdx.x; qq < q_end; qq += {cfg.block}) {{")
-        B("  const float4 q4 = sorted[qq];")
+        B("  int qq = item.y + threadIdx.x;")
+        B("  float4 q4n = qq < q_end ? __ldg(&sorted[qq]) : make_float4(0.f, 0.f, 0.f, 0.f);")
+        B(f"  for (; qq < q_end; qq += {cfg.block}) {{")
+        B("  const float4 q4 = q4n;")
+        B(f"  if (qq + {cfg.block} < q_end) q4n = __ldg(&sorted[qq + {cfg.block}]);   // prefetch the next record")
         B("  const long long qi = (long long)__float_as_int(q4.w);")
         comps = ["x", "y", "z"]
         for d in range(s):
@@ -768,10 +777,16 @@ def generate(space, config: GenConfig | None = None, extents=None,
         # ---- per-sub fetch offsets
         if fetch_mode == "affine":
             gi = 0 if same_geom else geo
-            L(f"const int* aff = &sg_aff{gi}[sub * {s + 1}];")
-            for e in range(s):
-                L(f"const int sp{e} = aff[{e}];")
-            L(f"const int boff = base + aff[{s}];")
+            if s == 3:
+                L(f"const int4 aff = *reinterpret_cast<const int4*>(&sg_aff{gi}[sub * 4]);")
+                for e, comp in zip(range(3), "xyz"):
+                    L(f"const int sp{e} = aff.{comp};")
+                L("const int boff = base + aff.w;")
+            else:
+                L(f"const int* aff = &sg_aff{gi}[sub * {s + 1}];")
+                for e in range(s):
+                    L(f"const int sp{e} = aff[{e}];")
+                L(f"const int boff = base + aff[{s}];")
             vals = {e: sorted({site[e] for site in t.ref_stencil}) for e in range(s)}
             for e in range(s):
                 for v in vals[e]:
@@ -807,6 +822,14 @@ def generate(space, config: GenConfig | None = None, extents=None,
 
         def emit_u(tag):
             us = []
+            if tq:
+                for d in range(3):
+                    L(f"const float4 tq{d}{tag} = *reinterpret_cast<const float4*>(&sg_Tq[sub * 12 + {4 * d}]);")
+                    name = f"u{d}{tag}"
+                    L(f"const float {name} = tq{d}{tag}.x * xf0 + tq{d}{tag}.y * xf1 + "
+                      f"tq{d}{tag}.z * xf2 + tq{d}{tag}.w;")
+                    us.append(name)
+                return us
             for d in range(s):
                 if t.uniform_T:
                     row = t.transforms[0][d]
@@ -891,7 +914,10 @@ def generate(space, config: GenConfig | None = None, extents=None,
                         parts.append(du[a] if w == 1 else (f"(-{du[a]})" if w == -1
                                                            else f"{flit(w, fw)} * {du[a]}"))
                     else:
-                        parts.append(f"sg_T[sub * {s * s} + {a * s + e}] * {du[a]}")
+                        if tq:
+                            parts.append(f"sg_Tq[sub * 12 + {4 * a + e}] * {du[a]}")
+                        else:
+                            parts.append(f"sg_T[sub * {s * s} + {a * s + e}] * {du[a]}")
                 if parts:
                     L(f"gacc{e} += {' + '.join(parts)};")
 

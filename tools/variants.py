@@ -25,14 +25,12 @@ VARIANTS = {
     "binned_auto_t256": dict(mode="binned", block=256, unroll_cosets=False),
     "binned_auto_t256_unroll": dict(mode="binned", block=256, unroll_cosets=True),
     "binned_auto_t512": dict(mode="binned", block=512, unroll_cosets=False),
-    "binned_auto_t256_c2048": dict(mode="binned", block=256, unroll_cosets=False, chunk=2048),
-    "binned_auto_t256_c8192": dict(mode="binned", block=256, unroll_cosets=False, chunk=8192),
-    "binned_b8_t256": dict(mode="binned", block=256, unroll_cosets=False, bin=8),
-    "binned_b12_t256": dict(mode="binned", block=256, unroll_cosets=False, bin=12),
-    "binned_auto_ldg": dict(mode="binned", block=256, unroll_cosets=False, stage="ldg"),
-    "binned_auto_sites": dict(mode="binned", block=256, unroll_cosets=False, form="sites"),
+    "binned_auto_t512_unroll": dict(mode="binned", block=512, unroll_cosets=True),
+    "binned_auto_t512_unroll_mb2": dict(mode="binned", block=512, unroll_cosets=True, min_blocks=2),
+    "binned_b12_t256_unroll": dict(mode="binned", block=256, unroll_cosets=True, bin=12),
+    "binned_b12_t384_unroll": dict(mode="binned", block=384, unroll_cosets=True, bin=12),
     "binned_auto_sites_unroll": dict(mode="binned", block=256, unroll_cosets=True, form="sites"),
-    "binned_auto_table": dict(mode="binned", block=256, unroll_cosets=False, coeffs="table"),
+    "binned_auto_t256_unroll_c16k": dict(mode="binned", block=256, unroll_cosets=True, chunk=16384),
 }
 
 
