@@ -164,7 +164,7 @@ __device__ __forceinline__ int sg_bin_of(const float* __restrict__ xs, long long
 }
 
 constexpr int SG_SORT_THREADS = 1024;
-constexpr int SG_SMEM_BINS = 4096;      // bins that fit the privatized shared histograms
+constexpr int SG_SMEM_BINS = 16384;     // bins that fit the privatized shared histograms
 constexpr int SG_SCAN_TILE = 8192;      // elements per CTA in the device-wide scan
 
 __device__ __forceinline__ int sg_bin_xyz(float x, float y, float z, const BinGeom& g) {
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(SG_SORT_THREADS) sg_bin_count(
   const long long lo = (long long)blockIdx.x * per;
   const long long hi = min(n, lo + per);
   sg_for_queries(xs, lo, hi, g, [&](long long, float x, float y, float z) {
-    sg_agg_add(hist, sg_bin_xyz(x, y, z, g));
+    atomicAdd(&hist[sg_bin_xyz(x, y, z, g)], 1);
   });
   __syncthreads();
   for (int b = threadIdx.x; b < g.nbins; b += blockDim.x) mat[(long long)b * G + blockIdx.x] = hist[b];
@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(SG_SORT_THREADS) sg_bin_scatter(
   const long long lo = (long long)blockIdx.x * per;
   const long long hi = min(n, lo + per);
   sg_for_queries(xs, lo, hi, g, [&](long long i, float x, float y, float z) {
-    const int pos = sg_agg_add(cnt, sg_bin_xyz(x, y, z, g));
+    const int pos = atomicAdd(&cnt[sg_bin_xyz(x, y, z, g)], 1);
     sorted[pos] = make_float4(x, y, z, __int_as_float((int)i));
   });
 }

@@ -308,6 +308,20 @@ class CudaProgram:
         return np.float32 if self.float_width == F32 else np.float64
 
 
+def _table_bytes(space, t: Tables, cfg) -> int:
+    """Upper estimate of the per-CTA shared-memory tables (sigma, transforms, offsets, LUT)."""
+    b = 0
+    if len(t.sigma) <= 4096:
+        b += 4 * len(t.sigma)
+    b += 4 * 12 * t.nsub            # transforms + t'
+    b += 4 * (t.n + 1) * t.nsub     # stencil offsets (table mode)
+    b += 4 * t.nsub                 # psi
+    if cfg.coeffs == "table":
+        nm = len({e for rp in space.ref_polys for (e, _c) in rp.poly.terms})
+        b += 4 * t.K * (t.n + 1) * (-(-nm // 4) * 4)
+    return b
+
+
 def _chunk_trees(space, cfg, t: Tables):
     """Per reference polynomial: per chunk, the tree to evaluate (or None)."""
     n = t.n
@@ -388,15 +402,17 @@ def generate(space, config: GenConfig | None = None, extents=None,
         margin = h + 2   # f32 binning may be off by one cell; rounding/cosets add one more
         H = margin
         unit = 4  # TMA: innermost box extent x 4 B must be a multiple of 16 B
+        tbytes = _table_bytes(space, t, cfg)
+        budget = max(16 * 1024, cfg.brick_budget - tbytes)
         if bin_ == 0:   # largest multiple of 4 whose bricks (all cosets) fit the budget
             bin_ = 4
-            while M * 4 * (-(-(bin_ + 4 + 2 * margin) // unit) * unit) ** s <= cfg.brick_budget \
+            while M * 4 * (-(-(bin_ + 4 + 2 * margin) // unit) * unit) ** s <= budget \
                     and bin_ + 4 <= max(ext[0]):
                 bin_ += 4
         if bin_ % 4:
             raise ValueError("bin must be a multiple of 4 (TMA box coordinates must be 16-B aligned)")
         nb = [-(-e // bin_) for e in ext[0]]
-        while int(np.prod(nb)) > 4096:         # the binning kernels' shared histogram limit
+        while int(np.prod(nb)) > 16384:        # the binning kernels' shared histogram limit
             bin_ += 4
             nb = [-(-e // bin_) for e in ext[0]]
         # TMA boxes: every extent a multiple of 4 elements and start coordinates multiples
@@ -722,16 +738,20 @@ def generate(space, config: GenConfig | None = None, extents=None,
         # ---- membership (codegen.py:230-250; oracle dot = left-to-right)
         if space.planes:
             L("unsigned q = 0u;")
+            dots = {}   # one fp64 dot product per distinct normal (planes share families)
             for i, (nrm, off) in enumerate(t.planes):
-                acc = None
-                for e in range(s):
-                    w = nrm[e]
-                    if w == 0:
-                        continue
-                    term = f"xc{e}" if w == 1 else (f"(-xc{e})" if w == -1
-                                                      else f"__dmul_rn(xc{e}, {dlit(w)})")
-                    acc = term if acc is None else f"__dadd_rn({acc}, {term})"
-                L(f"q |= (({acc or '0.0'}) >= {dlit(off)}) ? {1 << i}u : 0u;")
+                if nrm not in dots:
+                    acc = None
+                    for e in range(s):
+                        w = nrm[e]
+                        if w == 0:
+                            continue
+                        term = f"xc{e}" if w == 1 else (f"(-xc{e})" if w == -1
+                                                          else f"__dmul_rn(xc{e}, {dlit(w)})")
+                        acc = term if acc is None else f"__dadd_rn({acc}, {term})"
+                    dots[nrm] = f"dn{len(dots)}"
+                    L(f"const double {dots[nrm]} = {acc or '0.0'};")
+                L(f"q |= ({dots[nrm]} >= {dlit(off)}) ? {1 << i}u : 0u;")
             if t.compress:
                 L(f"q = q % {P}u;")
             if sigma_global:

@@ -255,42 +255,58 @@ class Producer:
                     out.append(n)
         return out
 
-    def _overlaps(self, R, n):
-        """Does some term's zonotope, shifted by n, meet the region's interior?"""
+    def _zonotope_hrep(self, dirs, mult, shift):
+        """(normals (k x s floats), lo, hi) with lo <= a.(x - shift) <= hi on the zonotope."""
         s = self.s
-        A, b = R.arrays()
-        for t in self.phi.terms:
-            bx = t.box
-            zc = []
-            for combo in itertools.combinations(range(len(bx.dirs)), s - 1):
-                vecs = [bx.dirs[i] for i in combo]
+        key = (tuple(dirs), tuple(mult), tuple(shift))
+        cache = self.__dict__.setdefault("_hrep_cache", {})
+        if key in cache:
+            return cache[key]
+        from .boxspline import _normal
+        rows, los, his = [], [], []
+        if s == 1:
+            lo = sum(m * d[0] for d, m in zip(dirs, mult) if d[0] < 0)
+            hi = sum(m * d[0] for d, m in zip(dirs, mult) if d[0] > 0)
+            rows, los, his = [[1.0]], [float(lo)], [float(hi)]
+        else:
+            seen = set()
+            for combo in itertools.combinations(range(len(dirs)), s - 1):
+                vecs = [dirs[i] for i in combo]
                 if _rank(vecs, s) < s - 1:
                     continue
-                from .boxspline import _normal
                 a = _normal(vecs, s)
-                lo = sum(a[d] * (t.shift[d] + n[d]) for d in range(s))
-                hi = lo
-                for d_, m in zip(bx.dirs, bx.mult):
+                if a in seen:
+                    continue
+                seen.add(a)
+                lo = hi = F(0)
+                for d_, m in zip(dirs, mult):
                     ad = sum(x * y for x, y in zip(a, d_))
                     if ad < 0:
                         lo += m * ad
                     else:
                         hi += m * ad
-                zc.append(([-float(v) for v in a], -float(lo)))
-                zc.append(([float(v) for v in a], float(hi)))
-            if s == 1:
-                lo = t.shift[0] + n[0]
-                hi = lo
-                for d_, m in zip(bx.dirs, bx.mult):
-                    if d_[0] < 0:
-                        lo += m * d_[0]
-                    else:
-                        hi += m * d_[0]
-                zc = [([-1.0], -float(lo)), ([1.0], float(hi))]
-            Az = np.array([z[0] for z in zc])
-            bz = np.array([z[1] for z in zc])
-            AA = np.vstack([A, Az])
-            bb = np.concatenate([b, bz])
+                rows.append([float(v) for v in a])
+                los.append(float(lo))
+                his.append(float(hi))
+        out = (np.array(rows), np.array(los), np.array(his),
+               np.array([float(v) for v in shift]))
+        cache[key] = out
+        return out
+
+    def _overlaps(self, R, n):
+        """Does phi(. - n)'s support (a term zonotope, or the hull zonotope when the
+        basis function declares one) meet the region's interior?"""
+        s = self.s
+        A, b = R.arrays()
+        hull = getattr(self.phi, "hull", None)
+        shapes = [hull] if hull is not None else [(t.box.dirs, t.box.mult, t.shift)
+                                                  for t in self.phi.terms]
+        nv = np.array([float(v) for v in n])
+        for dirs, mult, shift in shapes:
+            Z, lo, hi, sh = self._zonotope_hrep(dirs, mult, shift)
+            off = Z @ (sh + nv)
+            AA = np.vstack([A, -Z, Z])
+            bb = np.concatenate([b, -(lo + off), hi + off])
             norms = np.linalg.norm(AA, axis=1)
             c = np.zeros(s + 1)
             c[-1] = -1

@@ -89,7 +89,10 @@ def voronoi_spline(gens, order: int) -> BoxSum:
             bx = BoxSpline([gens[i] for i in used], [mult[i] for i in used])
             boxes[mult] = bx
         terms.append(BoxTerm(w, bx, shift))
-    return BoxSum(s, terms)
+    out = BoxSum(s, terms)
+    # support of V_k: the zonotope of every generator taken k times, centred at 0
+    out.hull = (tuple(gens), tuple([order] * len(gens)), tuple(-order * c for c in center))
+    return out
 
 
 H = F(1, 4)

@@ -1,0 +1,81 @@
+"""Parity at the benchmark configurations' full sizes (needs a B200).
+
+Size-independent properties on the full volumes and query streams of bench.py's
+configs (partition of unity, linearity in the data, periodic shift invariance),
+plus an oracle spot check on a subsample of the same workload.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import bench  # noqa: E402
+from oracle import refeval  # noqa: E402
+from paper_2102_08518_b200 import Evaluator  # noqa: E402
+from paper_2102_08518_b200.model import SPACES_DIR  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+CFGS = ["c1", "c2", "c3", "c4"]
+NQ = 1 << 20
+
+
+def _setup(cfg, ones=False):
+    dev = torch.device("cuda", 0)
+    space, arrays, _ = bench.make_inputs(cfg, 0, dev)
+    xs = bench.make_queries(cfg, 0, NQ, dev)
+    if ones:
+        arrays = [np.ones_like(a) for a in arrays]
+    _, prog = bench.build_program(cfg)
+    return space, arrays, xs, prog
+
+
+@pytest.mark.parametrize("cfg", CFGS)
+def test_partition_of_unity_full_size(cfg):
+    space, arrays, xs, prog = _setup(cfg, ones=True)
+    ev = Evaluator(space, arrays, prog=prog)
+    out = ev(xs)
+    out = out[0] if isinstance(out, tuple) else out
+    assert float((out - 1).abs().max()) <= 2e-5
+
+
+@pytest.mark.parametrize("cfg", CFGS)
+def test_linearity_full_size(cfg):
+    space, arrays, xs, prog = _setup(cfg)
+    rng = np.random.default_rng(11)
+    other = [rng.random(a.shape).astype(np.float32) for a in arrays]
+    mix = [(0.25 * a + 0.5 * b).astype(np.float32) for a, b in zip(arrays, other)]
+    outs = []
+    for data in (arrays, other, mix):
+        r = Evaluator(space, data, prog=prog)(xs)
+        outs.append((r[0] if isinstance(r, tuple) else r).double())
+    lhs = outs[2]
+    rhs = 0.25 * outs[0] + 0.5 * outs[1]
+    assert float((lhs - rhs).abs().max()) <= 1e-5
+
+
+@pytest.mark.parametrize("cfg", CFGS)
+def test_oracle_spot_check_full_size(cfg):
+    space, arrays, xs, prog = _setup(cfg)
+    ev = Evaluator(space, arrays, prog=prog)
+    r = ev(xs)
+    got = (r[0] if isinstance(r, tuple) else r)[:1500].double().cpu().numpy()
+    osp = refeval.load_space_file(SPACES_DIR / f"{space.name}.json")
+    sample = xs[:1500].double().cpu().numpy()
+    grad = prog.has_grad
+    ref = refeval.reference_eval_batch(osp, sample, [a.astype(np.float64) for a in arrays], grad=grad)
+    want = ref[0] if grad else ref
+    assert np.all(np.abs(got - want) <= 1e-6 + 1e-5 * np.maximum(np.abs(got), np.abs(want)))
+    if grad:
+        g = r[1][:1500].double().cpu().numpy()
+        assert np.abs(g - ref[1]).max() <= 1e-5 * max(1.0, float(np.abs(ref[1]).max()))
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3"])
+def test_direct_and_binned_agree_full_size(cfg):
+    space, arrays, xs, prog = _setup(cfg)
+    a = Evaluator(space, arrays, prog=prog)(xs)
+    _, p2 = bench.build_program(cfg, mode="direct")
+    b = Evaluator(space, arrays, prog=p2)(xs)
+    assert torch.equal(a, b) or float((a - b).abs().max()) <= 1e-6
