@@ -76,8 +76,8 @@ class GenConfig:
             raise ValueError("block must be a multiple of 32 in [32, 1024]")
         if self.mode not in ("direct", "binned"):
             raise ValueError("mode must be 'direct' or 'binned'")
-        if self.stage not in ("tma", "ldg"):
-            raise ValueError("stage must be 'tma' or 'ldg'")
+        if self.stage not in ("tma", "ldg", "l1"):
+            raise ValueError("stage must be 'tma', 'ldg' or 'l1' (no staging: sorted queries, L1 gathers)")
 
 
 def default_config(space: SplineSpace, **kw) -> GenConfig:
@@ -443,9 +443,12 @@ def generate(space, config: GenConfig | None = None, extents=None,
             st[d] = st[d + 1] * row[d + 1]
         strides.append(st)
     same_geom = len(set(pext)) == 1
-    if binned:
+    smem_fetch = binned and cfg.stage != "l1"
+    if smem_fetch:
         strides = [list(bstr) for _ in range(M)]   # fetch offsets are brick-relative
         same_geom = True
+    if binned and not smem_fetch:
+        smem_bytes = 0
 
     fw = cfg.float_width
     em = Emitter(fw)
@@ -601,7 +604,9 @@ def generate(space, config: GenConfig | None = None, extents=None,
         gst = [1] * s
         for d in range(s - 2, -1, -1):
             gst[d] = gst[d + 1] * pext[0][d + 1]
-        if cfg.stage == "tma":
+        if cfg.stage == "l1":
+            pass
+        elif cfg.stage == "tma":
             coords = ", ".join(f"%{2 + i}" for i in range(s))
             cvals = ", ".join(f'"r"(lo{d})' for d in range(s - 1, -1, -1))
             B("  const unsigned sg_bar_a = (unsigned)__cvta_generic_to_shared(&sg_bar);")
@@ -640,7 +645,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
         for name, ctype, vals in smem:
             B(f"  for (int i_ = threadIdx.x; i_ < {len(vals)}; i_ += {cfg.block}) {name}[i_] = {name}_c[i_];")
         B("  __syncthreads();")
-        if cfg.stage == "tma":
+        if cfg.stage == "tma" and smem_fetch:
             B('  asm volatile("{\\n .reg .pred p;\\n SG_WAIT_%=:\\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\\n @!p bra SG_WAIT_%=;\\n}" :: "r"(sg_bar_a) : "memory");')
         B(f"  const int q_end = min(starts[bin + 1], item.y + {cfg.chunk});")
         B("  int qq = item.y + threadIdx.x;")
@@ -677,7 +682,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
         """Body for coset `l` (int) or the loop variable `l` (dyn=True)."""
         L = em.line
         if dyn:
-            if binned:
+            if smem_fetch:
                 L(f"const float* V = sg_brick + l * {brick_elems};")
             else:
                 ptr = f"(const {T}*)vol.base[0]"
@@ -694,7 +699,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
                         expr = f"(l == {c} ? {dlit(t.cosets[c][d])} : {expr})"
                     L(f"const double xl{d} = __dsub_rn(x{d}, {expr});")
         else:
-            if binned:
+            if smem_fetch:
                 L(f"const float* V = sg_brick + {l * brick_elems};")
             else:
                 L(f"const {T}* __restrict__ V = (const {T}*)vol.base[{l}];")
@@ -784,7 +789,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
             raise ValueError("rolled coset loop needs equal coset extents")
         e_ = ext[geo]
         st_ = strides[geo]
-        if binned:
+        if smem_fetch:
             for d in range(s):
                 L(f"const int kw{d} = (int)(k{d} + rel{d});")
         else:
@@ -890,7 +895,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
             for step in plan.steps:
                 if step.kind == FETCH:
                     j = step.index
-                    if binned:
+                    if smem_fetch:
                         L(f"const {T} c{j}{tag} = V[{off_expr(j)}];")
                     else:
                         L(f"const {T} c{j}{tag} = __ldg(V + ({off_expr(j)}));")
@@ -982,7 +987,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
             for step in plan.steps:
                 if step.kind == FETCH:
                     j = step.index
-                    if binned:
+                    if smem_fetch:
                         L(f"const {T} c{j} = V[{off_expr(j)}];")
                     else:
                         L(f"const {T} c{j} = __ldg(V + ({off_expr(j)}));")

@@ -22,15 +22,13 @@ from paper_2102_08518_b200 import runtime  # noqa: E402
 
 VARIANTS = {
     "direct": dict(mode="direct", block=128),
-    "binned_auto_t256": dict(mode="binned", block=256, unroll_cosets=False),
     "binned_auto_t256_unroll": dict(mode="binned", block=256, unroll_cosets=True),
-    "binned_auto_t512": dict(mode="binned", block=512, unroll_cosets=False),
-    "binned_auto_t512_unroll": dict(mode="binned", block=512, unroll_cosets=True),
-    "binned_auto_t512_unroll_mb2": dict(mode="binned", block=512, unroll_cosets=True, min_blocks=2),
     "binned_b12_t256_unroll": dict(mode="binned", block=256, unroll_cosets=True, bin=12),
-    "binned_b12_t384_unroll": dict(mode="binned", block=384, unroll_cosets=True, bin=12),
-    "binned_auto_sites_unroll": dict(mode="binned", block=256, unroll_cosets=True, form="sites"),
-    "binned_auto_t256_unroll_c16k": dict(mode="binned", block=256, unroll_cosets=True, chunk=16384),
+    "binned_b8_t256_unroll": dict(mode="binned", block=256, unroll_cosets=True, bin=8),
+    "sorted_l1_b8_t128": dict(mode="binned", stage="l1", block=128, unroll_cosets=True, bin=8),
+    "sorted_l1_b8_t256": dict(mode="binned", stage="l1", block=256, unroll_cosets=True, bin=8),
+    "sorted_l1_b16_t256": dict(mode="binned", stage="l1", block=256, unroll_cosets=True, bin=16),
+    "sorted_l1_b8_t256_loop": dict(mode="binned", stage="l1", block=256, unroll_cosets=False, bin=8),
 }
 
 
