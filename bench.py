@@ -71,7 +71,7 @@ def gen_config_for(space, grad=False, **over):
     from paper_2102_08518_b200 import GenConfig, ScheduleParams
     n = space.stencil_size
     kw = dict(params=ScheduleParams(1, n, "predicated"), float_width="f32",
-              unroll_cosets=space.ncosets == 1, form="horner", block=256, grad=grad,
+              unroll_cosets=True, form="horner", block=256, grad=grad,
               mode="binned", coeffs="table" if space.nref > 2 else "imm")
     kw.update(over)
     return GenConfig(**kw)

@@ -86,5 +86,20 @@ def _fcc_box6():
     return _produce(centered_box(FCC_DIRS), FCC_COSETS, FCC_GEN, "fcc_box6")
 
 
+@register("bcc_voronoi2", (8, 8, 8))
+def _bcc_voronoi2():
+    """C3/C5: BCC Voronoi spline of order 2 (truncated-octahedron cell convolved with
+    itself; piecewise cubic), via the zonotopal tiling of the cell (voronoi.py)."""
+    from .voronoi import BCC_VORONOI_GENS, voronoi_spline
+    return _produce(voronoi_spline(BCC_VORONOI_GENS, 2), BCC_COSETS, BCC_GEN, "bcc_voronoi2")
+
+
+@register("fcc_voronoi2", (6, 6, 6))
+def _fcc_voronoi2():
+    """FCC Voronoi spline of order 2 (rhombic-dodecahedron cell; piecewise cubic)."""
+    from .voronoi import FCC_VORONOI_GENS, voronoi_spline
+    return _produce(voronoi_spline(FCC_VORONOI_GENS, 2), FCC_COSETS, FCC_GEN, "fcc_voronoi2")
+
+
 if __name__ == "__main__":
     raise SystemExit(main(sys.argv[1:]))
