@@ -106,6 +106,13 @@ int sg_module_regs(const sg_module* m, int* regs_per_thread, int* local_bytes);
  * Returns SG_EUNREACHABLE if any point hit sigma == -1 since the last call. */
 int sg_module_status(sg_module* m, void* stream, uint32_t* flags);
 
+/* Kernel timing for roofline reporting: while enabled, sg_eval brackets the evaluation
+ * kernel (not the binning kernels) with CUDA events on the launch stream;
+ * sg_module_kernel_time synchronizes them and returns the summed milliseconds and the
+ * number of launches since the last call (then resets). */
+int sg_module_timing(sg_module* m, int enable);
+int sg_module_kernel_time(sg_module* m, double* total_ms, int64_t* launches);
+
 /* extents: ncosets x dim (row-major); src[c] points to coset c's C-order array of
  * prod(extents[c]) elements, in HOST memory (src_on_device == 0) or device memory.
  * The device copy is periodic: padded element i holds src[(i - halo) mod E] on every

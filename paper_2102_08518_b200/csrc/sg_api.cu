@@ -93,7 +93,33 @@ struct sg_module {
   size_t bin_scratch_bytes = 0;
   int64_t nbins = 0;
   int64_t nb[SG_MAX_DIM] = {1, 1, 1, 1};
+  // optional event timing of the evaluation kernel
+  bool timing = false;
+  std::mutex t_mu;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> t_events;
+  size_t t_used = 0;
 };
+
+static int timed_launch(sg_module* m, const void* func, dim3 grid, dim3 block, void** args,
+                        size_t smem, cudaStream_t st) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (m->timing) {
+    std::lock_guard<std::mutex> lock(m->t_mu);
+    if (m->t_used == m->t_events.size()) {
+      cudaEvent_t a, b;
+      CU(cudaEventCreate(&a));
+      CU(cudaEventCreate(&b));
+      m->t_events.emplace_back(a, b);
+    }
+    e0 = m->t_events[m->t_used].first;
+    e1 = m->t_events[m->t_used].second;
+    ++m->t_used;
+    CU(cudaEventRecord(e0, st));
+  }
+  CU(cudaLaunchKernel(func, grid, block, args, smem, st));
+  if (e1) CU(cudaEventRecord(e1, st));
+  return SG_OK;
+}
 
 struct sg_volume {
   int device = 0;
@@ -359,6 +385,94 @@ __global__ void __launch_bounds__(SG_SORT_THREADS) sg_bin_scatter(
   });
 }
 
+// K3': tile-local counting sort before the scatter: records of one bin leave the CTA as
+// contiguous runs (coalesced 16-B stores) instead of one scattered store per query.
+constexpr int SG_TILE = 4096;
+constexpr int SG_TILED_MAX_BINS = 4096;
+
+__global__ void __launch_bounds__(1024) sg_bin_scatter_tiled(
+    const float* __restrict__ xs, long long n, long long per, BinGeom g,
+    const int* __restrict__ mat, float4* __restrict__ sorted) {
+  extern __shared__ __align__(16) unsigned char shb[];
+  const int nb = (int)g.nbins;
+  float4* tile = reinterpret_cast<float4*>(shb);                 // SG_TILE records
+  int* tbin = reinterpret_cast<int*>(tile + SG_TILE);              // SG_TILE bins
+  int* gpos = tbin + SG_TILE;                                      // nb: global cursor
+  int* lcnt = gpos + nb;                                           // nb: tile counts
+  int* loff = lcnt + nb;                                           // nb: tile offsets
+  __shared__ int scan_sh[32];
+  const int G = gridDim.x;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) gpos[b] = mat[(long long)b * G + blockIdx.x];
+  const long long lo = (long long)blockIdx.x * per;
+  const long long hi = min(n, lo + per);
+  const bool vec = g.dim == 3 && ((((uintptr_t)xs) & 15) == 0);
+  for (long long t0 = lo; t0 < hi; t0 += SG_TILE) {
+    const int tn = (int)min((long long)SG_TILE, hi - t0);
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) lcnt[b] = 0;
+    __syncthreads();
+    // A: 4 consecutive queries per thread (one float4 triple when aligned)
+    float4 rec[4];
+    int bb[4], rk[4];
+    const int q0 = threadIdx.x * 4;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) bb[k] = -1;
+    if (q0 < tn) {
+      const long long i0 = t0 + q0;
+      if (vec && q0 + 4 <= tn) {
+        const float4* X4 = reinterpret_cast<const float4*>(xs + i0 * 3);
+        const float4 a = X4[0], b = X4[1], c = X4[2];
+        rec[0] = make_float4(a.x, a.y, a.z, __int_as_float((int)i0));
+        rec[1] = make_float4(a.w, b.x, b.y, __int_as_float((int)(i0 + 1)));
+        rec[2] = make_float4(b.z, b.w, c.x, __int_as_float((int)(i0 + 2)));
+        rec[3] = make_float4(c.y, c.z, c.w, __int_as_float((int)(i0 + 3)));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) bb[k] = sg_bin_xyz(rec[k].x, rec[k].y, rec[k].z, g);
+      } else {
+        for (int k = 0; k < 4 && q0 + k < tn; ++k) {
+          const long long i = i0 + k;
+          rec[k] = make_float4(xs[i * g.dim], g.dim > 1 ? xs[i * g.dim + 1] : 0.f,
+                               g.dim > 2 ? xs[i * g.dim + 2] : 0.f, __int_as_float((int)i));
+          bb[k] = sg_bin_xyz(rec[k].x, rec[k].y, rec[k].z, g);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (bb[k] >= 0) rk[k] = atomicAdd(&lcnt[bb[k]], 1);
+    __syncthreads();
+    // B: tile offsets (exclusive scan over bins)
+    {
+      const int per_t = (nb + 1023) / 1024;
+      const int b0 = threadIdx.x * per_t, b1 = min(nb, b0 + per_t);
+      int mine = 0;
+      for (int b = b0; b < b1; ++b) mine += lcnt[b];
+      int at = sg_block_excl_scan(mine, scan_sh, nullptr);
+      for (int b = b0; b < b1; ++b) {
+        loff[b] = at;
+        at += lcnt[b];
+      }
+    }
+    __syncthreads();
+    // C: place records bin-contiguously in the tile
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (bb[k] >= 0) {
+        const int slot = loff[bb[k]] + rk[k];
+        tile[slot] = rec[k];
+        tbin[slot] = bb[k];
+      }
+    __syncthreads();
+    // D: coalesced runs to the global positions
+    for (int j = threadIdx.x; j < tn; j += blockDim.x) {
+      const int b = tbin[j];
+      sorted[gpos[b] + (j - loff[b])] = tile[j];
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) gpos[b] += lcnt[b];
+    __syncthreads();
+  }
+}
+
 extern "C" {
 
 int sg_version(void) { return SG_VERSION; }
@@ -501,9 +615,35 @@ int sg_module_free(sg_module* m) {
     if (s) cudaStreamDestroy(s);
   if (m->scratch) cudaFree(m->scratch);
   if (m->bin_scratch) cudaFree(m->bin_scratch);
+  for (auto& pr : m->t_events) {
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
   if (m->d_err) cudaFree(m->d_err);
   if (m->lib) cudaLibraryUnload(m->lib);
   delete m;
+  return SG_OK;
+}
+
+int sg_module_timing(sg_module* m, int enable) {
+  if (!m) return fail(SG_EINVAL, "NULL module");
+  m->timing = enable != 0;
+  return SG_OK;
+}
+
+int sg_module_kernel_time(sg_module* m, double* total_ms, int64_t* launches) {
+  if (!m) return fail(SG_EINVAL, "NULL module");
+  std::lock_guard<std::mutex> lock(m->t_mu);
+  double tot = 0;
+  for (size_t i = 0; i < m->t_used; ++i) {
+    CU(cudaEventSynchronize(m->t_events[i].second));
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, m->t_events[i].first, m->t_events[i].second));
+    tot += ms;
+  }
+  if (total_ms) *total_ms = tot;
+  if (launches) *launches = (int64_t)m->t_used;
+  m->t_used = 0;
   return SG_OK;
 }
 
@@ -737,6 +877,9 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
                          2 * SG_SMEM_BINS * sizeof(int));
     cudaFuncSetAttribute(sg_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          SG_SMEM_BINS * sizeof(int));
+    cudaFuncSetAttribute(sg_bin_scatter_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         SG_TILE * (sizeof(float4) + sizeof(int)) +
+                             3 * SG_TILED_MAX_BINS * sizeof(int));
   });
   sg_bin_count<<<(unsigned)G, SG_SORT_THREADS, nb * sizeof(int), st>>>((const float*)xs, (long long)n,
                                                                       per, g, mat);
@@ -748,8 +891,14 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
                                                               starts);
   CU(cudaGetLastError());
   sg_make_items<<<1, 1024, 0, st>>>(starts, (int)nb, chunk, items, (int)max_items);
-  sg_bin_scatter<<<(unsigned)G, SG_SORT_THREADS, nb * sizeof(int), st>>>(
-      (const float*)xs, (long long)n, per, g, mat, sorted);
+  if (nb <= (size_t)SG_TILED_MAX_BINS) {
+    const size_t shb = SG_TILE * (sizeof(float4) + sizeof(int)) + 3 * nb * sizeof(int);
+    sg_bin_scatter_tiled<<<(unsigned)G, 1024, shb, st>>>((const float*)xs, (long long)n, per, g,
+                                                        mat, sorted);
+  } else {
+    sg_bin_scatter<<<(unsigned)G, SG_SORT_THREADS, nb * sizeof(int), st>>>(
+        (const float*)xs, (long long)n, per, g, mat, sorted);
+  }
   CU(cudaGetLastError());
   SgCosets cs{};
   for (int c = 0; c < v->ncosets; ++c) cs.base[c] = v->origin[c];
@@ -784,8 +933,8 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
   const void* itp = items;
   void* args[] = {(void*)&sp, (void*)&stp, (void*)&itp, (void*)&out, (void*)&grad, (void*)&dbg,
                   (void*)&err, (void*)&cs, (void*)&tm};
-  CU(cudaLaunchKernel((const void*)m->kernel, dim3((unsigned)max_items), dim3(in.block), args,
-                      (size_t)in.smem_bytes, st));
+  return timed_launch(m, (const void*)m->kernel, dim3((unsigned)max_items), dim3(in.block), args,
+                      (size_t)in.smem_bytes, st);
   return SG_OK;
 }
 
@@ -802,8 +951,8 @@ static int launch(sg_module* m, const sg_volume* v, const void* xs, int64_t n, v
   long long per_block = (long long)m->info.block * m->info.queries_per_thread;
   long long grid = (nn + per_block - 1) / per_block;
   if (grid > 0x7fffffffLL) return fail(SG_EINVAL, "batch too large for one launch");
-  CU(cudaLaunchKernel((const void*)m->kernel, dim3((unsigned)grid), dim3(m->info.block), args, 0,
-                      st));
+  return timed_launch(m, (const void*)m->kernel, dim3((unsigned)grid), dim3(m->info.block), args, 0,
+                      st);
   return SG_OK;
 }
 

@@ -82,6 +82,9 @@ EXPORTS = {
                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "sg_eval_host": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64], ctypes.c_int),
+    "sg_module_timing": ([ctypes.c_void_p, ctypes.c_int], ctypes.c_int),
+    "sg_module_kernel_time": ([ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
+                               ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
     "sg_volume_replicate": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
                              ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
 }
@@ -202,6 +205,15 @@ class Module:
         r, lb = ctypes.c_int(), ctypes.c_int()
         _check(lib().sg_module_regs(self.handle, ctypes.byref(r), ctypes.byref(lb)))
         return r.value, lb.value
+
+    def set_timing(self, enable: bool):
+        _check(lib().sg_module_timing(self.handle, int(enable)))
+
+    def kernel_time(self):
+        """(summed ms, launches) of the evaluation kernel since the last call."""
+        ms, n = ctypes.c_double(), ctypes.c_int64()
+        _check(lib().sg_module_kernel_time(self.handle, ctypes.byref(ms), ctypes.byref(n)))
+        return ms.value, n.value
 
     def status(self, stream=None):
         f = ctypes.c_uint32()
