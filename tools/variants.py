@@ -25,10 +25,13 @@ VARIANTS = {
     "binned_auto_t256_unroll": dict(mode="binned", block=256, unroll_cosets=True),
     "binned_b12_t256_unroll": dict(mode="binned", block=256, unroll_cosets=True, bin=12),
     "binned_b8_t256_unroll": dict(mode="binned", block=256, unroll_cosets=True, bin=8),
-    "sorted_l1_b8_t128": dict(mode="binned", stage="l1", block=128, unroll_cosets=True, bin=8),
+    "binned_auto_t256_loop": dict(mode="binned", block=256, unroll_cosets=False),
     "sorted_l1_b8_t256": dict(mode="binned", stage="l1", block=256, unroll_cosets=True, bin=8),
-    "sorted_l1_b16_t256": dict(mode="binned", stage="l1", block=256, unroll_cosets=True, bin=16),
-    "sorted_l1_b8_t256_loop": dict(mode="binned", stage="l1", block=256, unroll_cosets=False, bin=8),
+    "direct_table": dict(mode="direct", block=128, coeffs="table"),
+    "direct_imm_pred": dict(mode="direct", block=128, coeffs="imm"),
+    "direct_imm_branchy": dict(mode="direct", block=128, coeffs="imm", branchy=True),
+    "binned_imm_pred": dict(mode="binned", block=256, coeffs="imm"),
+    "binned_table_b8": dict(mode="binned", block=256, coeffs="table", bin=8),
 }
 
 
@@ -43,32 +46,39 @@ def main():
     space, arrays, xs = bench.make_inputs(a.config, 0, dev)
     n = xs.shape[0]
     out = torch.empty(n, device=dev)
+    grad = torch.empty((n, space.dim), device=dev)
     ref = None
     for name, over in VARIANTS.items():
         if a.only and a.only not in name:
             continue
         try:
+            over = dict(over)
+            if over.pop("branchy", False):
+                from paper_2102_08518_b200 import ScheduleParams
+                over["params"] = ScheduleParams(1, space.stencil_size, "branchy")
             _, prog = bench.build_program(a.config, **over)
             ev = Evaluator(space, arrays, prog=prog)
         except Exception as e:  # noqa: BLE001
             print(f"{name:28s} FAILED {e}")
             continue
         for _ in range(3):
-            runtime.eval_device(ev.module, ev.volume, xs, out)
+            runtime.eval_device(ev.module, ev.volume, xs, out, grad if prog.has_grad else None)
         torch.cuda.synchronize()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record()
         for _ in range(a.reps):
-            runtime.eval_device(ev.module, ev.volume, xs, out)
+            runtime.eval_device(ev.module, ev.volume, xs, out, grad if prog.has_grad else None)
         s1.record()
         torch.cuda.synchronize()
         ms = s0.elapsed_time(s1) / a.reps
+        ev.module.set_timing(False)
+        kms, kn = ev.module.kernel_time()
         ev.module.status()
         if ref is None:
             ref = out.clone()
         diff = float((out - ref).abs().max())
-        print(f"{name:28s} {ms:8.4f} ms  {n / ms / 1e6:8.3f} Grecon/s  regs {ev.module.regs()[0]:3d}"
-              f"  maxdiff-vs-first {diff:.2e}", flush=True)
+        print(f"{name:28s} {ms:8.4f} ms (eval {kms / max(kn, 1):7.4f})  {n / ms / 1e6:8.3f} Grecon/s"
+              f"  regs {ev.module.regs()[0]:3d}  maxdiff-vs-first {diff:.2e}", flush=True)
 
 
 if __name__ == "__main__":
