@@ -950,7 +950,11 @@ static int launch(sg_module* m, const sg_volume* v, const void* xs, int64_t n, v
                   (void*)&cs};
   long long per_block = (long long)m->info.block * m->info.queries_per_thread;
   long long grid = (nn + per_block - 1) / per_block;
-  if (grid > 0x7fffffffLL) return fail(SG_EINVAL, "batch too large for one launch");
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device);
+  // grid-stride kernel: about four full waves, so per-CTA table staging is amortized
+  const long long cap = (long long)sms * std::max(1, 2048 / m->info.block) * 4;
+  grid = std::min(grid, cap);
   return timed_launch(m, (const void*)m->kernel, dim3((unsigned)grid), dim3(m->info.block), args, 0,
                       st);
   return SG_OK;

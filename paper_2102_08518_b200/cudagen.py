@@ -575,8 +575,9 @@ def generate(space, config: GenConfig | None = None, extents=None,
             B(f"  for (int i_ = threadIdx.x; i_ < {len(vals)}; i_ += {cfg.block}) {name}[i_] = {name}_c[i_];")
         if smem:
             B("  __syncthreads();")
-        B(f"  const long long qi = (long long)blockIdx.x * {cfg.block} + threadIdx.x;")
-        B("  if (qi >= n) return;")
+        # grid-stride loop: the shared tables are staged once per CTA, not once per 128 queries
+        B(f"  for (long long qi = (long long)blockIdx.x * {cfg.block} + threadIdx.x; qi < n;")
+        B(f"       qi += (long long)gridDim.x * {cfg.block}) {{")
         for d in range(s):
             B(f"  const double x{d} = (double)xs[qi * {s} + {d}];")
         ind = "  "
@@ -1074,8 +1075,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
     if cfg.grad:
         for d in range(s):
             body.append(f"  grad[qi * {s} + {d}] = gacc{d};")
-    if binned:
-        body.append("  }")
+    body.append("  }")   # query loop (grid-stride in direct mode, chunk loop in binned mode)
     body.append("}")
     if lut:
         lit = ", ".join(flit(Fraction(v), fw) for v in lut)

@@ -22,16 +22,15 @@ from paper_2102_08518_b200 import runtime  # noqa: E402
 
 VARIANTS = {
     "direct": dict(mode="direct", block=128),
+    "direct_b256": dict(mode="direct", block=256),
+    "direct_imm_branchy": dict(mode="direct", block=128, coeffs="imm", branchy=True),
+    "direct_table": dict(mode="direct", block=128, coeffs="table"),
     "binned_auto_t256_unroll": dict(mode="binned", block=256, unroll_cosets=True),
     "binned_b12_t256_unroll": dict(mode="binned", block=256, unroll_cosets=True, bin=12),
-    "binned_b8_t256_unroll": dict(mode="binned", block=256, unroll_cosets=True, bin=8),
-    "binned_auto_t256_loop": dict(mode="binned", block=256, unroll_cosets=False),
-    "sorted_l1_b8_t256": dict(mode="binned", stage="l1", block=256, unroll_cosets=True, bin=8),
-    "direct_table": dict(mode="direct", block=128, coeffs="table"),
-    "direct_imm_pred": dict(mode="direct", block=128, coeffs="imm"),
-    "direct_imm_branchy": dict(mode="direct", block=128, coeffs="imm", branchy=True),
     "binned_imm_pred": dict(mode="binned", block=256, coeffs="imm"),
-    "binned_table_b8": dict(mode="binned", block=256, coeffs="table", bin=8),
+    "binned_imm_branchy": dict(mode="binned", block=256, coeffs="imm", branchy=True),
+    "binned_table": dict(mode="binned", block=256, coeffs="table"),
+    "sorted_l1_imm": dict(mode="binned", stage="l1", block=256, coeffs="imm"),
 }
 
 
@@ -65,6 +64,8 @@ def main():
             runtime.eval_device(ev.module, ev.volume, xs, out, grad if prog.has_grad else None)
         torch.cuda.synchronize()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev.module.kernel_time()
+        ev.module.set_timing(True)
         s0.record()
         for _ in range(a.reps):
             runtime.eval_device(ev.module, ev.volume, xs, out, grad if prog.has_grad else None)
