@@ -521,15 +521,21 @@ def generate(space, config: GenConfig | None = None, extents=None,
         nm = len(exps)
         nmp = -(-nm // 4) * 4
         midx = {e: i for i, e in enumerate(exps)}
-        Atab = [0.0] * (t.K * t.n * nmp)
+        # per-psi block stride padded to an odd number of 16-B groups, so the LDS.128 of
+        # threads holding different reference polynomials spread over the smem banks
+        pstride = t.n * nmp
+        if (pstride // 4) % 2 == 0:
+            pstride += 4
+        Atab = [0.0] * (t.K * pstride)
         A0tab = [0.0] * (t.K * nmp)
         for k_, rp in enumerate(space.ref_polys):
             for (e, c), q in rp.poly.terms.items():
                 if c == NO_SYMBOL:
                     A0tab[k_ * nmp + midx[e]] = q
                 else:
-                    Atab[(k_ * t.n + c) * nmp + midx[e]] = q
-        tab = dict(exps=exps, nm=nm, nmp=nmp, has_free=any(v != 0 for v in A0tab))
+                    Atab[k_ * pstride + c * nmp + midx[e]] = q
+        tab = dict(exps=exps, nm=nm, nmp=nmp, pstride=pstride,
+                   has_free=any(v != 0 for v in A0tab))
         smem.append(("sg_A", T, Atab))
         if tab["has_free"]:
             smem.append(("sg_A0", T, A0tab))
@@ -980,7 +986,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
             vec = "float4" if T == "float" else "double2"
             w = 4 if T == "float" else 2
             comps = ["x", "y", "z", "w"][:w]
-            L(f"const {vec}* __restrict__ Arow = reinterpret_cast<const {vec}*>(&sg_A[{psi_e} * {t.n * nmp}]);")
+            L(f"const {vec}* __restrict__ Arow = reinterpret_cast<const {vec}*>(&sg_A[{psi_e} * {tab['pstride']}]);")
             for m in range(nmp):
                 L(f"{T} g{m} = ({T})0;")
             u = None
