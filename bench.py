@@ -39,19 +39,21 @@ PROFILES = ROOT / "profiles"
 # name -> workload (BASELINE.json configs, restated concretely in SURVEY.md 8d)
 CONFIGS = {
     "c1": dict(space="tricubic", extents=(64, 64, 64), queries=1 << 20, kind="uniform",
-               grad=False, scaling="weak",
+               grad=False, scaling="weak", variant=dict(mode="binned"),
                desc="tensor-product tricubic B-spline on Z^3, 64^3, 2^20 uniform"),
     "c2": dict(space="bcc_box5", extents=(101, 101, 101), queries=1 << 24, kind="uniform",
-               grad=False, scaling="weak",
+               grad=False, scaling="weak", variant=dict(mode="binned", coeffs="imm"),
                desc="BCC quintic box spline (4 dirs x2), 2x101^3 coset-split, 2^24 uniform"),
     "c3": dict(space="bcc_voronoi2", extents=(203, 203, 203), queries=1 << 26, kind="rays",
                rays=(512, 512, 256), grad=False, scaling="weak",
+               variant=dict(mode="direct", coeffs="imm", block=128),
                desc="BCC Voronoi spline (order 2, piecewise cubic), 2x203^3, 2^26 ray-ordered"),
     "c4": dict(space="fcc_box6", extents=(161, 161, 161), queries=1 << 26, kind="uniform",
-               grad=True, scaling="weak",
+               grad=True, scaling="weak", variant=dict(mode="direct", coeffs="imm", block=128),
                desc="FCC 6-direction box spline, 4x161^3, 2^26 uniform, value + gradient"),
     "c5": dict(space="bcc_voronoi2", extents=(406, 406, 406), queries=1 << 30, kind="rays",
                rays=(1024, 1024, 1024), grad=False, scaling="strong",
+               variant=dict(mode="direct", coeffs="imm", block=128),
                desc="BCC Voronoi spline (order 2), 2x406^3, 2^30 ray-ordered sharded over the GPUs"),
 }
 DEFAULT_CONFIG = "c2"
@@ -78,10 +80,13 @@ def gen_config_for(space, grad=False, **over):
 
 
 def build_program(cfg_name, **over):
+    """The configuration's measured-best variant (CONFIGS[..]['variant']), plus overrides."""
     from paper_2102_08518_b200 import generate, load_fixture
     c = CONFIGS[cfg_name]
     space = load_fixture(c["space"])
-    return space, generate(space, gen_config_for(space, c["grad"], **over), c["extents"])
+    kw = dict(c.get("variant", {}))
+    kw.update(over)
+    return space, generate(space, gen_config_for(space, c["grad"], **kw), c["extents"])
 
 
 def precompile_bench_kernels():
@@ -233,15 +238,24 @@ def query_range(cfg_name, rank, world):
     return rank * c["queries"], (rank + 1) * c["queries"]
 
 
-def make_queries(cfg_name, lo, hi, device):
+def make_queries(cfg_name, lo, hi, device, chunk=1 << 25):
+    """Queries [lo, hi) of the configuration's global stream, generated in chunks on
+    `device` (the generators use fp64 temporaries; chunking bounds their footprint)."""
+    import torch
     from paper_2102_08518_b200 import queries
     c = CONFIGS[cfg_name]
-    if c["kind"] == "rays":
-        w, h, st = c["rays"]
-        total = w * h * st
-        # weak-scaled ranks beyond the first replay the ray stream (same work per rank)
-        return queries.rays(lo % total, lo % total + (hi - lo), c["extents"], w, h, st, 2, device)
-    return queries.uniform(lo, hi, c["extents"], 1, device)
+    out = torch.empty((hi - lo, len(c["extents"])), dtype=torch.float32, device=device)
+    for a in range(lo, hi, chunk):
+        b = min(hi, a + chunk)
+        if c["kind"] == "rays":
+            w, h, st = c["rays"]
+            total = w * h * st
+            # weak-scaled ranks beyond the first replay the ray stream (same work per rank)
+            a0 = a % total
+            out[a - lo:b - lo] = queries.rays(a0, a0 + (b - a), c["extents"], w, h, st, 2, device)
+        else:
+            out[a - lo:b - lo] = queries.uniform(a, b, c["extents"], 1, device)
+    return out
 
 
 def make_inputs(cfg_name, rank, device, world=1):
