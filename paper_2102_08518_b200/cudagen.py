@@ -43,7 +43,7 @@ from .schedule import BRANCHY, COMPUTE, FETCH, PREDICATED, ScheduleParams, sched
 F64 = "f64"
 F32 = "f32"
 ENTRY = "sg_eval_kernel"
-FORMS = ("horner", "sites")
+FORMS = ("horner", "sites", "sym")
 COEFFS = ("imm", "lut", "table")
 
 
@@ -454,8 +454,22 @@ def generate(space, config: GenConfig | None = None, extents=None,
     em = Emitter(fw)
     T = em.T
     P = t.modulus
-    trees = _chunk_trees(space, cfg, t)
+    symforms = None
+    if cfg.form == "sym":
+        from .symmetry import symmetrize
+        symforms = []
+        for i, rp in enumerate(space.ref_polys):
+            sub = next(sb for sb in space.subregions if sb.psi_index == i)
+            symforms.append(symmetrize(rp.poly, sub.stencil))
+    trees = _chunk_trees(space, cfg if cfg.form != "sym" else replace(cfg, form="horner"), t)
     gtrees = _grad_trees(space, cfg, t) if cfg.grad else None
+    if symforms is not None:
+        sym_trees = [horner_factorize(f.poly) if f is not None else None for f in symforms]
+        sym_gtrees = None
+        if cfg.grad:
+            sym_gtrees = [[horner_factorize(f.poly.differentiate(a)) if f is not None
+                           and f.poly.differentiate(a) else None for a in range(t.s)]
+                          if f is not None else None for f in symforms]
     plans = [schedule_pipeline(group_polynomial(space.ref_polys[sb.psi_index].poly,
                                                 cfg.params.group_size, range(t.n)), cfg.params)
              for sb in space.subregions]
@@ -895,7 +909,73 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 L("const int psi = sg_psi[sub];")
         cvars = [f"c{j}" for j in range(t.n)]
 
+        def run_plan_sym(psis, tag):
+            """All fetches in plan order, then per psi the symmetry-mixed symbols and
+            one Horner evaluation of psi'(v, s) (form "sym")."""
+            for step in plan.steps:
+                if step.kind == FETCH:
+                    j = step.index
+                    if smem_fetch:
+                        L(f"const {T} c{j}{tag} = V[{off_expr(j)}];")
+                    else:
+                        L(f"const {T} c{j}{tag} = __ldg(V + ({off_expr(j)}));")
+            u = emit_u(tag)
+            accs, grads = {}, ({} if cfg.grad else None)
+            for i in psis:
+                f = symforms[i]
+                cv = [f"c{j}{tag}" for j in range(t.n)]
+                if f is None:
+                    v = em.tree(horner_factorize(space.ref_polys[i].poly), u, cv, consts)
+                    accs[i] = v
+                    if cfg.grad:
+                        grads[i] = [em.tree(gtrees[i][a], u, cv, consts) if gtrees[i][a] is not None
+                                    else f"({T})0" for a in range(s)]
+                    continue
+                vv = []
+                for d in range(s):
+                    if f.shift[d] != 0:
+                        nm = em.tmp("v")
+                        L(f"const {T} {nm} = {u[d]} - {flit(f.shift[d], fw)};")
+                        vv.append(nm)
+                    else:
+                        vv.append(u[d])
+                sv = [None] * len(f.mixes)
+                kk = len(f.axes)
+                for reps, syms in f.orbits:
+                    if len(reps) == 1 << kk:
+                        # free orbit: fast Walsh-Hadamard butterflies over the flip group
+                        x = {bits: cv[j] for bits, j in reps}
+                        for tb in range(kk):
+                            nx = {}
+                            for b in x:
+                                if b >> tb & 1:
+                                    continue
+                                hi = b | (1 << tb)
+                                a_, b_ = em.tmp("w"), em.tmp("w")
+                                L(f"const {T} {a_} = {x[b]} + {x[hi]};")
+                                L(f"const {T} {b_} = {x[b]} - {x[hi]};")
+                                nx[b], nx[hi] = a_, b_
+                            x = nx
+                        for P, k_ in syms.items():
+                            sv[k_] = x[P]
+                    else:
+                        for P, k_ in syms.items():
+                            expr = ""
+                            for sign, j in f.mixes[k_]:
+                                expr += (" + " if sign > 0 else " - ") + cv[j] if expr else (
+                                    cv[j] if sign > 0 else f"-{cv[j]}")
+                            nm = em.tmp("s")
+                            L(f"const {T} {nm} = {expr};")
+                            sv[k_] = nm
+                accs[i] = em.tree(sym_trees[i], vv, sv, consts)
+                if cfg.grad:
+                    grads[i] = [em.tree(sym_gtrees[i][a], vv, sv, consts)
+                                if sym_gtrees[i][a] is not None else f"({T})0" for a in range(s)]
+            return accs, grads, u
+
         def run_plan(psis, tag):
+            if symforms is not None:
+                return run_plan_sym(psis, tag)
             accs = {i: None for i in psis}
             u = None
             nchunk = 0

@@ -66,6 +66,8 @@ CONFIGS = [
     dict(mode="binned", form="sites", block=256),
     dict(coeffs="table"),
     dict(coeffs="table", mode="binned", params_md=(2, 4)),
+    dict(form="sym"),
+    dict(form="sym", mode="binned", params_mode="branchy"),
 ]
 
 
@@ -106,7 +108,7 @@ def test_values_f64_variant(name):
 
 
 @pytest.mark.parametrize("name", golden_names())
-@pytest.mark.parametrize("mode", ["direct", "binned", "table"])
+@pytest.mark.parametrize("mode", ["direct", "binned", "table", "sym"])
 def test_gradient_vs_oracle(name, mode):
     space, ospace, z, arrays = load_golden(name)
     xs = z["uniform_xs"].astype(np.float64)
@@ -114,6 +116,8 @@ def test_gradient_vs_oracle(name, mode):
                                             grad=True)
     if mode == "table":
         ev = _evaluator(space, arrays, grad=True, coeffs="table")
+    elif mode == "sym":
+        ev = _evaluator(space, arrays, grad=True, form="sym")
     else:
         ev = _evaluator(space, arrays, grad=True, mode=mode)
     out, g, _ = ev(_xs(z, "uniform"))

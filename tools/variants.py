@@ -21,19 +21,13 @@ from paper_2102_08518_b200 import Evaluator, load_fixture  # noqa: E402
 from paper_2102_08518_b200 import runtime  # noqa: E402
 
 VARIANTS = {
+    "default": dict(),
+    "sym": dict(form="sym"),
+    "sym_b12": dict(form="sym", bin=12),
+    "sym_t512": dict(form="sym", block=512),
+    "sym_direct": dict(form="sym", mode="direct", block=128),
+    "sym_l1": dict(form="sym", mode="binned", stage="l1", block=256),
     "direct": dict(mode="direct", block=128),
-    "direct_imm_branchy": dict(mode="direct", block=128, coeffs="imm", branchy=True),
-    "direct_imm_pred": dict(mode="direct", block=128, coeffs="imm"),
-    "direct_table": dict(mode="direct", block=128, coeffs="table"),
-    "binned_auto_t256_unroll": dict(mode="binned", block=256, unroll_cosets=True),
-    "binned_b12_t256_unroll": dict(mode="binned", block=256, unroll_cosets=True, bin=12),
-    "binned_imm_pred": dict(mode="binned", block=256, coeffs="imm"),
-    "binned_imm_pred_b12": dict(mode="binned", block=256, coeffs="imm", bin=12),
-    "binned_table": dict(mode="binned", block=256, coeffs="table"),
-    "binned_table_b12": dict(mode="binned", block=256, coeffs="table", bin=12),
-    "sorted_l1_imm": dict(mode="binned", stage="l1", block=256, coeffs="imm"),
-    "sorted_l1_table": dict(mode="binned", stage="l1", block=256, coeffs="table"),
-    "sorted_l1_table_b12": dict(mode="binned", stage="l1", block=256, coeffs="table", bin=12),
 }
 
 
