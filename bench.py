@@ -39,10 +39,11 @@ PROFILES = ROOT / "profiles"
 # name -> workload (BASELINE.json configs, restated concretely in SURVEY.md 8d)
 CONFIGS = {
     "c1": dict(space="tricubic", extents=(64, 64, 64), queries=1 << 20, kind="uniform",
-               grad=False, scaling="weak", variant=dict(mode="binned"),
+               grad=False, scaling="weak", variant=dict(mode="binned", form="sym"),
                desc="tensor-product tricubic B-spline on Z^3, 64^3, 2^20 uniform"),
     "c2": dict(space="bcc_box5", extents=(101, 101, 101), queries=1 << 24, kind="uniform",
-               grad=False, scaling="weak", variant=dict(mode="binned", coeffs="imm"),
+               grad=False, scaling="weak",
+               variant=dict(mode="binned", coeffs="imm", form="sym", block=512),
                desc="BCC quintic box spline (4 dirs x2), 2x101^3 coset-split, 2^24 uniform"),
     "c3": dict(space="bcc_voronoi2", extents=(203, 203, 203), queries=1 << 26, kind="rays",
                rays=(512, 512, 256), grad=False, scaling="weak",
