@@ -385,6 +385,38 @@ __global__ void __launch_bounds__(SG_SORT_THREADS) sg_bin_scatter(
   });
 }
 
+// fused small scan (one CTA): exclusive scan of the (bin, CTA) matrix, bin starts and
+// the evaluation work items -- replaces 5 launches when the matrix is small
+__global__ void __launch_bounds__(1024) sg_bin_scan_small(int* __restrict__ mat, long long mlen,
+                                                          int nbins, int G, long long n, int chunk,
+                                                          int* __restrict__ starts,
+                                                          int2* __restrict__ items, int max_items) {
+  __shared__ int sh[32];
+  const long long per = (mlen + 1023) / 1024;
+  const long long lo = threadIdx.x * per, hi = min(mlen, lo + per);
+  int mine = 0;
+  for (long long i = lo; i < hi; ++i) mine += mat[i];
+  int run = sg_block_excl_scan(mine, sh, nullptr);
+  for (long long i = lo; i < hi; ++i) {
+    const int v = mat[i];
+    mat[i] = run;
+    run += v;
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbins; b += 1024) starts[b] = mat[(long long)b * G];
+  if (threadIdx.x == 0) starts[nbins] = (int)n;
+  __syncthreads();
+  const int pb = (nbins + 1023) / 1024;
+  const int b0 = threadIdx.x * pb, b1 = min(nbins, b0 + pb);
+  int nchunks = 0;
+  for (int b = b0; b < b1; ++b) nchunks += (starts[b + 1] - starts[b] + chunk - 1) / chunk;
+  int total;
+  int at = sg_block_excl_scan(nchunks, sh, &total);
+  for (int b = b0; b < b1; ++b)
+    for (int q = starts[b]; q < starts[b + 1]; q += chunk) items[at++] = make_int2(b, q);
+  for (int i = total + threadIdx.x; i < max_items; i += 1024) items[i] = make_int2(-1, 0);
+}
+
 // K3': tile-local counting sort before the scatter: records of one bin leave the CTA as
 // contiguous runs (coalesced 16-B stores) instead of one scattered store per query.
 constexpr int SG_TILE = 4096;
@@ -406,21 +438,38 @@ __global__ void __launch_bounds__(1024) sg_bin_scatter_tiled(
   const long long lo = (long long)blockIdx.x * per;
   const long long hi = min(n, lo + per);
   const bool vec = g.dim == 3 && ((((uintptr_t)xs) & 15) == 0);
+  const int q0 = threadIdx.x * 4;
+  // software pipeline: the next tile's query triple is loaded while this tile is sorted
+  float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pb = pa, pc = pa;
+  if (vec && lo + q0 + 4 <= hi) {
+    const float4* X4 = reinterpret_cast<const float4*>(xs + (lo + q0) * 3);
+    pa = X4[0];
+    pb = X4[1];
+    pc = X4[2];
+  }
   for (long long t0 = lo; t0 < hi; t0 += SG_TILE) {
     const int tn = (int)min((long long)SG_TILE, hi - t0);
+    const float4 ca = pa, cb = pb, cc = pc;
+    {
+      const long long nx = t0 + SG_TILE + q0;
+      if (vec && nx + 4 <= hi) {
+        const float4* X4 = reinterpret_cast<const float4*>(xs + nx * 3);
+        pa = __ldg(X4);
+        pb = __ldg(X4 + 1);
+        pc = __ldg(X4 + 2);
+      }
+    }
     for (int b = threadIdx.x; b < nb; b += blockDim.x) lcnt[b] = 0;
     __syncthreads();
     // A: 4 consecutive queries per thread (one float4 triple when aligned)
     float4 rec[4];
     int bb[4], rk[4];
-    const int q0 = threadIdx.x * 4;
 #pragma unroll
     for (int k = 0; k < 4; ++k) bb[k] = -1;
     if (q0 < tn) {
       const long long i0 = t0 + q0;
       if (vec && q0 + 4 <= tn) {
-        const float4* X4 = reinterpret_cast<const float4*>(xs + i0 * 3);
-        const float4 a = X4[0], b = X4[1], c = X4[2];
+        const float4 a = ca, b = cb, c = cc;
         rec[0] = make_float4(a.x, a.y, a.z, __int_as_float((int)i0));
         rec[1] = make_float4(a.w, b.x, b.y, __int_as_float((int)(i0 + 1)));
         rec[2] = make_float4(b.z, b.w, c.x, __int_as_float((int)(i0 + 2)));
@@ -884,13 +933,18 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
   sg_bin_count<<<(unsigned)G, SG_SORT_THREADS, nb * sizeof(int), st>>>((const float*)xs, (long long)n,
                                                                       per, g, mat);
   CU(cudaGetLastError());
-  sg_scan_tiles<<<(unsigned)ntiles, 1024, 0, st>>>(mat, mlen, tile_sums);
-  sg_scan_sums<<<1, 1024, 0, st>>>(tile_sums, ntiles);
-  sg_scan_apply<<<(unsigned)ntiles, 1024, 0, st>>>(mat, mlen, tile_sums);
-  sg_bin_starts<<<(unsigned)((nb + 256) / 256), 256, 0, st>>>(mat, (long long)nb, (int)G, (long long)n,
-                                                              starts);
+  if (mlen <= (1LL << 18)) {
+    sg_bin_scan_small<<<1, 1024, 0, st>>>(mat, mlen, (int)nb, (int)G, (long long)n, chunk, starts,
+                                          items, (int)max_items);
+  } else {
+    sg_scan_tiles<<<(unsigned)ntiles, 1024, 0, st>>>(mat, mlen, tile_sums);
+    sg_scan_sums<<<1, 1024, 0, st>>>(tile_sums, ntiles);
+    sg_scan_apply<<<(unsigned)ntiles, 1024, 0, st>>>(mat, mlen, tile_sums);
+    sg_bin_starts<<<(unsigned)((nb + 256) / 256), 256, 0, st>>>(mat, (long long)nb, (int)G,
+                                                                (long long)n, starts);
+    sg_make_items<<<1, 1024, 0, st>>>(starts, (int)nb, chunk, items, (int)max_items);
+  }
   CU(cudaGetLastError());
-  sg_make_items<<<1, 1024, 0, st>>>(starts, (int)nb, chunk, items, (int)max_items);
   if (nb <= (size_t)SG_TILED_MAX_BINS) {
     const size_t shb = SG_TILE * (sizeof(float4) + sizeof(int)) + 3 * nb * sizeof(int);
     sg_bin_scatter_tiled<<<(unsigned)G, 1024, shb, st>>>((const float*)xs, (long long)n, per, g,
