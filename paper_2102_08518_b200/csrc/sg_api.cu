@@ -933,7 +933,7 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
   sg_bin_count<<<(unsigned)G, SG_SORT_THREADS, nb * sizeof(int), st>>>((const float*)xs, (long long)n,
                                                                       per, g, mat);
   CU(cudaGetLastError());
-  if (mlen <= (1LL << 18)) {
+  if (mlen <= 16384) {   // a single CTA only wins for tiny matrices (latency-bound otherwise)
     sg_bin_scan_small<<<1, 1024, 0, st>>>(mat, mlen, (int)nb, (int)G, (long long)n, chunk, starts,
                                           items, (int)max_items);
   } else {
