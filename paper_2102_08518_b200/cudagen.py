@@ -683,9 +683,9 @@ def generate(space, config: GenConfig | None = None, extents=None,
         rnd0 = rm0.rounding if rm0.shape == PARALLELEPIPED else ROUND_NEAREST
         for d in range(s):
             if rnd0 == ROUND_NEAREST:
-                B(f"  const long long kb{d} = (long long)(x{d} >= 0.0 ? floor(__dadd_rn(x{d}, 0.5)) : ceil(__dsub_rn(x{d}, 0.5)));")
+                B(f"  const long long kb{d} = __double2ll_rz(__dadd_rn(x{d}, copysign(0.5, x{d})));")
             else:
-                B(f"  const long long kb{d} = (long long)floor(x{d});")
+                B(f"  const long long kb{d} = __double2ll_rd(x{d});")
             e_ = ext[0][d]
             B(f"  int kbw{d} = (int)kb{d};")
             B(f"  if ((unsigned)kbw{d} >= {e_}u) {{ long long m_ = kb{d} % {e_}LL; kbw{d} = (int)(m_ < 0 ? m_ + {e_}LL : m_); }}")
@@ -738,13 +738,15 @@ def generate(space, config: GenConfig | None = None, extents=None,
             basis, rounding = exact.eye(s), ROUND_NEAREST
 
         def rnd(v):
+            # round half away from zero == trunc(v + copysign(1/2, v)) with the same RN
+            # addition the oracle performs (floor(v+1/2) / ceil(v-1/2), oracle.py:34-35);
+            # converted to an integer in one cvt.rzi / cvt.rmi
             if rounding == ROUND_NEAREST:
-                return (f"(({v}) >= 0.0 ? floor(__dadd_rn(({v}), 0.5)) : "
-                        f"ceil(__dsub_rn(({v}), 0.5)))")
-            return f"floor({v})"
+                return f"__double2ll_rz(__dadd_rn(({v}), copysign(0.5, ({v}))))"
+            return f"__double2ll_rd({v})"
         if exact.is_identity(basis):
             for d in range(s):
-                L(f"const long long k{d} = (long long){rnd(f'xl{d}')};")
+                L(f"const long long k{d} = {rnd(f'xl{d}')};")
         else:
             inv = exact.inverse(basis)
             for d in range(s):
@@ -755,7 +757,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
                     term = f"xl{e}" if inv[d][e] == 1 else f"__dmul_rn(xl{e}, {dlit(inv[d][e])})"
                     acc = term if acc is None else f"__dadd_rn({acc}, {term})"
                 L(f"const double bu{d} = {acc or '0.0'};")
-                L(f"const long long r{d} = (long long){rnd(f'bu{d}')};")
+                L(f"const long long r{d} = {rnd(f'bu{d}')};")
             for d in range(s):
                 terms = [f"{int(basis[d][e])}LL * r{e}" for e in range(s) if basis[d][e] != 0]
                 L(f"const long long k{d} = {' + '.join(terms) or '0LL'};")
@@ -766,6 +768,15 @@ def generate(space, config: GenConfig | None = None, extents=None,
             L("unsigned q = 0u;")
             dots = {}   # one fp64 dot product per distinct normal (planes share families)
             for i, (nrm, off) in enumerate(t.planes):
+                nz = [(e, w) for e, w in enumerate(nrm) if w != 0]
+                if off == 0 and len(nz) == 2 and all(abs(w) == 1 for _, w in nz):
+                    # a.x >= 0 with two unit coefficients is an exact comparison:
+                    # RN(xa +- xb) >= 0  <=>  xa >= -+xb (sign of an IEEE sum is exact)
+                    (ea, wa), (eb, wb) = nz
+                    lhs = f"xc{ea}" if wa == 1 else f"(-xc{ea})"
+                    rhs = f"(-xc{eb})" if wb == 1 else f"xc{eb}"
+                    L(f"q |= ({lhs} >= {rhs}) ? {1 << i}u : 0u;")
+                    continue
                 if nrm not in dots:
                     acc = None
                     for e in range(s):
