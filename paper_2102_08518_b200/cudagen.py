@@ -767,7 +767,50 @@ def generate(space, config: GenConfig | None = None, extents=None,
         if space.planes:
             L("unsigned q = 0u;")
             dots = {}   # one fp64 dot product per distinct normal (planes share families)
+            fam_done = set()
+            # families of parallel planes with offsets m_1..m_r * 2^-p (consecutive integers
+            # m, contiguous increasing bits): the r bits are a threshold count,
+            # cnt = clamp(floor(dot * 2^p) - m_1 + 1, 0, r) -- exact, because dot * 2^p is
+            # exact and comparing with integers commutes with floor
+            fams = {}
             for i, (nrm, off) in enumerate(t.planes):
+                fams.setdefault(nrm, []).append((i, off))
+            counted = {}
+            for nrm, lst in fams.items():
+                if len(lst) < 3:
+                    continue
+                idxs = [i for i, _ in lst]
+                offs = [o for _, o in lst]
+                if idxs != list(range(idxs[0], idxs[0] + len(idxs))):
+                    continue
+                step = offs[1] - offs[0]
+                if step <= 0 or any(offs[k + 1] - offs[k] != step for k in range(len(offs) - 1)):
+                    continue
+                inv = 1 / step
+                if inv.denominator != 1 or int(inv) & (int(inv) - 1):
+                    continue   # spacing must be 2^-p so the scaling is exact
+                m1 = offs[0] * inv
+                if m1.denominator != 1:
+                    continue
+                counted[nrm] = (idxs[0], len(idxs), int(inv), int(m1))
+            for i, (nrm, off) in enumerate(t.planes):
+                if nrm in counted:
+                    if nrm in fam_done:
+                        continue
+                    fam_done.add(nrm)
+                    acc = None
+                    for e in range(s):
+                        w = nrm[e]
+                        if w == 0:
+                            continue
+                        term = f"xc{e}" if w == 1 else (f"(-xc{e})" if w == -1
+                                                          else f"__dmul_rn(xc{e}, {dlit(w)})")
+                        acc = term if acc is None else f"__dadd_rn({acc}, {term})"
+                    b0, r, sc, m1 = counted[nrm]
+                    cnt = em.tmp("cnt")
+                    L(f"const int {cnt} = min(max(__double2int_rd(({acc or '0.0'}) * {float(sc)!r}) - ({m1 - 1}), 0), {r});")
+                    L(f"q |= ((1u << {cnt}) - 1u) << {b0};")
+                    continue
                 nz = [(e, w) for e, w in enumerate(nrm) if w != 0]
                 if off == 0 and len(nz) == 2 and all(abs(w) == 1 for _, w in nz):
                     # a.x >= 0 with two unit coefficients is an exact comparison:
