@@ -535,20 +535,22 @@ def generate(space, config: GenConfig | None = None, extents=None,
         nm = len(exps)
         nmp = -(-nm // 4) * 4
         midx = {e: i for i, e in enumerate(exps)}
-        # per-psi block stride padded to an odd number of 16-B groups, so the LDS.128 of
-        # threads holding different reference polynomials spread over the smem banks
-        pstride = t.n * nmp
-        if (pstride // 4) % 2 == 0:
-            pstride += 4
-        Atab = [0.0] * (t.K * pstride)
+        # layout [site j][monomial quad q][psi][4]: for a fixed (j, q) the threads of a
+        # warp read consecutive 16-B chunks indexed by their own psi -> the LDS.128s are
+        # bank-conflict free (distinct psi) or broadcasts (equal psi), and the (j, q)
+        # offset is an immediate
+        w4 = 4 if T == "float" else 2
+        nq = nmp // w4
+        Atab = [0.0] * (t.n * nq * t.K * w4)
         A0tab = [0.0] * (t.K * nmp)
         for k_, rp in enumerate(space.ref_polys):
             for (e, c), q in rp.poly.terms.items():
                 if c == NO_SYMBOL:
                     A0tab[k_ * nmp + midx[e]] = q
                 else:
-                    Atab[k_ * pstride + c * nmp + midx[e]] = q
-        tab = dict(exps=exps, nm=nm, nmp=nmp, pstride=pstride,
+                    mi = midx[e]
+                    Atab[((c * nq + mi // w4) * t.K + k_) * w4 + mi % w4] = q
+        tab = dict(exps=exps, nm=nm, nmp=nmp, nq=nq,
                    has_free=any(v != 0 for v in A0tab))
         smem.append(("sg_A", T, Atab))
         if tab["has_free"]:
@@ -1120,7 +1122,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
             vec = "float4" if T == "float" else "double2"
             w = 4 if T == "float" else 2
             comps = ["x", "y", "z", "w"][:w]
-            L(f"const {vec}* __restrict__ Arow = reinterpret_cast<const {vec}*>(&sg_A[{psi_e} * {tab['pstride']}]);")
+            L(f"const {vec}* __restrict__ Arow = reinterpret_cast<const {vec}*>(sg_A) + {psi_e};")
             for m in range(nmp):
                 L(f"{T} g{m} = ({T})0;")
             u = None
@@ -1135,7 +1137,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 elif step.kind == COMPUTE:
                     for j in plan.blocks[step.index]:
                         for q in range(nmp // w):
-                            L(f"{{ const {vec} a_ = Arow[{(j * nmp) // w + q}]; " + " ".join(
+                            L(f"{{ const {vec} a_ = Arow[{(j * tab['nq'] + q) * t.K}]; " + " ".join(
                                 f"g{q * w + r} = a_.{comps[r]} * c{j} + g{q * w + r};" for r in range(w)) + " }")
                     nchunk += 1
             if tab["has_free"]:

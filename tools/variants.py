@@ -22,12 +22,10 @@ from paper_2102_08518_b200 import runtime  # noqa: E402
 
 VARIANTS = {
     "default": dict(),
-    "sym": dict(form="sym"),
-    "sym_b12": dict(form="sym", bin=12),
-    "sym_t512": dict(form="sym", block=512),
-    "sym_direct": dict(form="sym", mode="direct", block=128),
-    "sym_l1": dict(form="sym", mode="binned", stage="l1", block=256),
+    "table": dict(coeffs="table"),
+    "imm_pred": dict(coeffs="imm"),
     "direct": dict(mode="direct", block=128),
+    "sym": dict(form="sym"),
 }
 
 
