@@ -24,5 +24,19 @@ def test_cuda_sweep_zp():
     from tests.conftest import GOLDEN
     sp = load_space(GOLDEN / "spaces" / "zp.json")
     data = make_volume(sp, (64, 64), seed=0, float_width="f32")
-    recs = run_sweep(sp, data, grid=[(1, 7), (2, 4)], trials=1 << 16, batch_size=1 << 14)
+    from oracle import refeval
+    from paper_2102_08518_b200.model import serialize_space
+    osp = refeval.load_space(serialize_space(sp))
+    cells = []
+
+    def check(pts, got, cell):
+        want = refeval.reference_eval_batch(osp, pts, [np.asarray(a, np.float64) for a in data.arrays])
+        tol = cell[-1]
+        err = np.abs(got - want)
+        assert (err <= 1e-12 + tol * np.maximum(np.abs(got), np.abs(want))).all(), (cell, err.max())
+        cells.append(cell[:3])
+
+    recs = run_sweep(sp, data, grid=[(1, 7), (2, 4)], trials=1 << 16, batch_size=1 << 14,
+                     check=check)
     assert len(recs) == 4 and all(r.mean_recon_per_sec > 0 for r in recs)
+    assert len(cells) == 4

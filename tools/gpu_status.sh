@@ -1,0 +1,15 @@
+#!/bin/bash
+# Full status pass on one B200: build, smoke, GPU tests, bench lines for every config, variant timings.
+# usage (under gpurun, from the repo root): bash tools/gpu_status.sh <tag> [configs]
+TAG=${1:-r01}; CFGS=${2:-c2 c1 c3 c4}
+mkdir -p gpurun_out
+nvidia-smi -L
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" 2>&1 | tail -3
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -15
+for c in $CFGS; do
+  timeout 900 python bench.py --config $c > gpurun_out/bench_${c}_${TAG}.json 2> gpurun_out/bench_${c}_${TAG}.err
+  tail -c 400 gpurun_out/bench_${c}_${TAG}.json; echo; tail -3 gpurun_out/bench_${c}_${TAG}.err
+done
+for c in $CFGS; do
+  echo "== variants $c"; timeout 600 python tools/variants.py $c --reps 20 2>&1 | grep -E "Grecon|FAIL|Error"
+done
