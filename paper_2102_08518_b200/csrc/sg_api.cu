@@ -646,6 +646,16 @@ int sg_module_load(const void* image, size_t image_len, const char* entry, int d
       }
     }
   }
+  if (m->info.mode == SG_MODE_DIRECT && m->info.smem_bytes > 0) {
+    // sorted direct kernels keep their per-tile pair records in dynamic shared memory
+    e = cudaFuncSetAttribute((const void*)m->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             m->info.smem_bytes);
+    if (e != cudaSuccess) {
+      cudaLibraryUnload(m->lib);
+      delete m;
+      return fail(SG_ECUDA, "smem attribute: %s", cudaGetErrorString(e));
+    }
+  }
   e = cudaMalloc(&m->d_err, sizeof(unsigned));
   if (e == cudaSuccess) e = cudaMemset(m->d_err, 0, sizeof(unsigned));
   if (e != cudaSuccess) {
@@ -1006,11 +1016,20 @@ static int launch(sg_module* m, const sg_volume* v, const void* xs, int64_t n, v
   long long grid = (nn + per_block - 1) / per_block;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device);
-  // grid-stride kernel: about four full waves, so per-CTA table staging is amortized
-  const long long cap = (long long)sms * std::max(1, 2048 / m->info.block) * 4;
+  // grid-stride kernel: about four full waves, so per-CTA table staging is amortized;
+  // kernels with dynamic shared memory (sorted tiles) run one persistent wave
+  long long cap = (long long)sms * std::max(1, 2048 / m->info.block) * 4;
+  if (m->info.smem_bytes > 0) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)m->kernel, m->info.block,
+                                                      (size_t)m->info.smem_bytes) != cudaSuccess ||
+        occ < 1)
+      occ = 1;
+    cap = (long long)sms * occ;
+  }
   grid = std::min(grid, cap);
-  return timed_launch(m, (const void*)m->kernel, dim3((unsigned)grid), dim3(m->info.block), args, 0,
-                      st);
+  return timed_launch(m, (const void*)m->kernel, dim3((unsigned)grid), dim3(m->info.block), args,
+                      (size_t)std::max(0, m->info.smem_bytes), st);
   return SG_OK;
 }
 

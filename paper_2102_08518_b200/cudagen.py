@@ -64,6 +64,8 @@ class GenConfig:
     chunk: int = 4096            # binned: queries per CTA work item (a bin is split in chunks)
     brick_budget: int = 112 * 1024   # binned auto-bin: shared-memory budget for the bricks
     stage: str = "tma"           # binned: brick staging, "tma" (cp.async.bulk.tensor) | "ldg"
+    tile: int = 0                # sorted: queries per CTA tile (0 = auto: 2 CTAs / SM of smem)
+    select: str = "auto"         # selection arithmetic: "f64" | "int" (2^-30 fixed point) | "auto"
 
     def __post_init__(self):
         if self.float_width not in (F64, F32):
@@ -74,8 +76,12 @@ class GenConfig:
             raise ValueError(f"coeffs must be one of {COEFFS}")
         if self.block % 32 or not 32 <= self.block <= 1024:
             raise ValueError("block must be a multiple of 32 in [32, 1024]")
-        if self.mode not in ("direct", "binned"):
-            raise ValueError("mode must be 'direct' or 'binned'")
+        if self.mode not in ("direct", "binned", "sorted"):
+            raise ValueError("mode must be 'direct', 'binned' or 'sorted'")
+        if self.select not in ("auto", "f64", "int"):
+            raise ValueError("select must be 'auto', 'f64' or 'int'")
+        if self.mode == "sorted" and (self.tile % self.block or self.tile > 8192 or self.tile < 0):
+            raise ValueError("sorted mode: tile must be a multiple of block and <= 8192")
         if self.stage not in ("tma", "ldg", "l1"):
             raise ValueError("stage must be 'tma', 'ldg' or 'l1' (no staging: sorted queries, L1 gathers)")
 
@@ -224,6 +230,76 @@ def derive_tables(space: SplineSpace) -> Tables:
         affine=aff, ref_stencil=ref)
 
 
+def plane_families(t: Tables) -> dict:
+    """Families of parallel planes with offsets m_1..m_r * 2^-p (consecutive integers m,
+    contiguous increasing bits): their r bits are one threshold count,
+    cnt = clamp(floor(dot * 2^p) - m_1 + 1, 0, r) -- exact, because dot * 2^p is exact
+    and comparing with integers commutes with floor.  normal -> (bit0, r, 2^p, m_1)."""
+    fams = {}
+    for i, (nrm, off) in enumerate(t.planes):
+        fams.setdefault(nrm, []).append((i, off))
+    counted = {}
+    for nrm, lst in fams.items():
+        if len(lst) < 3:
+            continue
+        idxs = [i for i, _ in lst]
+        offs = [o for _, o in lst]
+        if idxs != list(range(idxs[0], idxs[0] + len(idxs))):
+            continue
+        step = offs[1] - offs[0]
+        if step <= 0 or any(offs[k + 1] - offs[k] != step for k in range(len(offs) - 1)):
+            continue
+        inv = 1 / step
+        if inv.denominator != 1 or int(inv) & (int(inv) - 1):
+            continue   # spacing must be 2^-p so the scaling is exact
+        m1 = offs[0] * inv
+        if m1.denominator != 1:
+            continue
+        counted[nrm] = (idxs[0], len(idxs), int(inv), int(m1))
+    return counted
+
+
+FIX = 30          # fixed-point fraction bits of the integer selection path
+FIX_MIN = 2.0 ** -7   # |x| >= 2^-7: an fp32 x is a multiple of 2^-30 (ulp(2^-7) = 2^-30)
+
+
+def int_selection_ok(space, t: Tables, fw: str) -> bool:
+    """Can rho + plane tests run exactly in 2^-30 fixed point (int32)?
+
+    For f32 queries x >= 2^-7 every quantity the fp64 oracle forms (x - l, the rounding,
+    x_loc, small-integer plane dots, dot * 2^p) is a multiple of 2^-30 that fp64 holds
+    exactly, so exact integer arithmetic on x * 2^30 reproduces it bit for bit
+    (oracle.py:34-74).  Needs: identity region basis, coset offsets m * 2^-30 in
+    [0, 1/2] (round) or [0, 1) (floor), integer plane normals and offsets m * 2^-30 with
+    every |dot| < 2^31, family spacings 2^-p with p <= 30."""
+    if fw != F32 or t.s > 3:
+        return False
+    rm = space.region_map
+    if rm.shape == PARALLELEPIPED:
+        if not exact.is_identity(rm.basis):
+            return False
+        rounding = rm.rounding
+    else:
+        rounding = ROUND_NEAREST
+    hi = Fraction(1, 2) if rounding == ROUND_NEAREST else Fraction(1)
+    for off in t.cosets:
+        for o in off:
+            if (o * 2 ** FIX).denominator != 1 or not (0 <= o <= hi) or (rounding != ROUND_NEAREST and o == 1):
+                return False
+    amp = 2 ** (FIX - 1) if rounding == ROUND_NEAREST else 2 ** FIX
+    for nrm, off in t.planes:
+        if any(Fraction(w).denominator != 1 for w in nrm):
+            return False
+        if (off * 2 ** FIX).denominator != 1 or abs(off) * 2 ** FIX >= 2 ** 31:
+            return False
+        if sum(abs(int(w)) for w in nrm) * amp >= 2 ** 31:   # |DOT| fits int32
+            return False
+    for nrm, (b0, r, sc, m1) in plane_families(t).items():
+        if sc > 2 ** FIX:
+            return False
+    return True
+
+
 # -- expression emission -------------------------------------------------------------
 
 
@@ -295,6 +371,7 @@ class CudaProgram:
     brick: tuple = ()
     smem_bytes: int = 0
     chunk: int = 0
+    queries_per_thread: int = 1   # sorted mode: tile / block (one CTA tile per grid step)
     stage_tma: bool = False
     rounding: int = 1
     meta: dict = field(default_factory=dict)
@@ -388,6 +465,21 @@ def generate(space, config: GenConfig | None = None, extents=None,
         raise ValueError(f"extents must give {s} values for each of {M} cosets")
     h = t.halo
     binned = cfg.mode == "binned"
+    sorted_ = cfg.mode == "sorted"
+    if sorted_:
+        if cfg.float_width != F32 or s > 3:
+            raise ValueError("sorted mode supports f32 kernels of dimension <= 3")
+        if not cfg.unroll_cosets:
+            raise ValueError("sorted mode unrolls the coset loop")
+        # per (query, coset) pair: record (u, base) 16 B + order 4 B + key/result 4 B
+        # (16 B result with the gradient); two CTAs per SM share the 227 KB
+        pair_bytes = 36 if cfg.grad else 24
+        if cfg.tile == 0:
+            tb = _table_bytes(space, t, cfg)
+            room = 110 * 1024 - tb
+            tq = max(cfg.block, min(8192, room // (M * pair_bytes)) // cfg.block * cfg.block)
+            tq = min(tq, max(cfg.block, 2048 // cfg.block * cfg.block))
+            cfg = replace(cfg, tile=tq)
     bin_ = cfg.bin
     rm0 = space.region_map
     if binned:
@@ -451,6 +543,10 @@ def generate(space, config: GenConfig | None = None, extents=None,
         smem_bytes = 0
 
     fw = cfg.float_width
+    intsel = cfg.select != "f64" and (M == 1 or cfg.unroll_cosets) and int_selection_ok(space, t, fw)
+    if cfg.select == "int" and not intsel:
+        raise ValueError("this space/variant cannot use the integer selection path")
+    families = plane_families(t)
     em = Emitter(fw)
     T = em.T
     P = t.modulus
@@ -584,7 +680,19 @@ def generate(space, config: GenConfig | None = None, extents=None,
         A(f"__device__ const int sg_sigma_g[{len(t.sigma)}] = {{{', '.join(str(v) for v in t.sigma)}}};")
 
     # ---- kernel -------------------------------------------------------------
-    lb = f"{cfg.block}, {cfg.min_blocks}" if cfg.min_blocks else f"{cfg.block}"
+    def int_prelude():
+        """Per query: fixed-point split x = hi + lo * 2^-30 (lo in [0, 2^30)), exact for the
+        fast-path range 2^-7 <= x < 2^30; other queries take the fp64 path."""
+        out = ["const bool fast_ = " + " && ".join(
+            f"(xq{d} >= 0x1p-7f) && (xq{d} < 0x1p+30f)" for d in range(s)) + ";"]
+        for d in range(s):
+            out.append(f"const long long X{d}_ = __float2ll_rn(xq{d} * 0x1p+30f);")
+            out.append(f"const int hi{d}_ = (int)(X{d}_ >> 30);")
+            out.append(f"const int lo{d}_ = (int)X{d}_ & 0x3fffffff;")
+        return out
+
+    min_blocks = cfg.min_blocks or (2 if sorted_ else 0)   # sorted: 2 CTAs / SM by design
+    lb = f"{cfg.block}, {min_blocks}" if min_blocks else f"{cfg.block}"
     body = []
     B = body.append
     if not binned:
@@ -595,14 +703,50 @@ def generate(space, config: GenConfig | None = None, extents=None,
             B(f"  __shared__ __align__(16) {ctype} {name}[{len(vals)}];")
         for name, ctype, vals in smem:
             B(f"  for (int i_ = threadIdx.x; i_ < {len(vals)}; i_ += {cfg.block}) {name}[i_] = {name}_c[i_];")
-        if smem:
+        if sorted_:
+            TQ = cfg.tile
+            MP = M * TQ
+            B("  extern __shared__ __align__(16) unsigned char sg_dyn[];")
+            B("  float4* sg_rec = reinterpret_cast<float4*>(sg_dyn);")
+            # the pair keys (rank | sub << 16) live in the result array until the scatter
+            if cfg.grad:
+                B(f"  float4* sg_res4 = reinterpret_cast<float4*>(sg_dyn + {MP * 16});")
+                B(f"  int* sg_key = reinterpret_cast<int*>(sg_dyn + {MP * 16});")
+                B(f"  int* sg_ord = reinterpret_cast<int*>(sg_dyn + {MP * 32});")
+            else:
+                B(f"  float* sg_res = reinterpret_cast<float*>(sg_dyn + {MP * 16});")
+                B(f"  int* sg_key = reinterpret_cast<int*>(sg_dyn + {MP * 16});")
+                B(f"  int* sg_ord = reinterpret_cast<int*>(sg_dyn + {MP * 20});")
+            B("  __shared__ int sg_cnt[32];")
+            B("  __shared__ int sg_start[32];")
+            B("  __shared__ int sg_tot;")
+            B("  if (threadIdx.x < 32) sg_cnt[threadIdx.x] = 0;")
+            B("  const unsigned lane = threadIdx.x & 31u;")
+            B("  const unsigned lt_mask = (1u << lane) - 1u;")
+            for l in range(M):
+                B(f"  const int coff{l} = (int)((const float*)vol.base[{l}] - (const float*)vol.base[0]);")
             B("  __syncthreads();")
-        # grid-stride loop: the shared tables are staged once per CTA, not once per 128 queries
-        B(f"  for (long long qi = (long long)blockIdx.x * {cfg.block} + threadIdx.x; qi < n;")
-        B(f"       qi += (long long)gridDim.x * {cfg.block}) {{")
-        for d in range(s):
-            B(f"  const double x{d} = (double)xs[qi * {s} + {d}];")
-        ind = "  "
+            # persistent tiles: the shared tables are staged once per CTA
+            B(f"  for (long long q0 = (long long)blockIdx.x * {TQ}; q0 < n; q0 += (long long)gridDim.x * {TQ}) {{")
+            sorted_smem = MP * pair_bytes
+            ind = "  "
+        elif smem:
+            B("  __syncthreads();")
+        if sorted_:
+            pass
+        else:
+          # grid-stride loop: the shared tables are staged once per CTA, not once per 128 queries
+          B(f"  for (long long qi = (long long)blockIdx.x * {cfg.block} + threadIdx.x; qi < n;")
+          B(f"       qi += (long long)gridDim.x * {cfg.block}) {{")
+          for d in range(s):
+              if intsel:
+                  B(f"  const float xq{d} = xs[qi * {s} + {d}];")
+                  B(f"  const double x{d} = (double)xq{d};")
+              else:
+                  B(f"  const double x{d} = (double)xs[qi * {s} + {d}];")
+          if intsel:
+              body.extend("  " + ln for ln in int_prelude())
+          ind = "  "
     else:
         B(f'extern "C" __global__ void __launch_bounds__({lb}) {ENTRY}(')
         B("    const float4* __restrict__ sorted, const int* __restrict__ starts,")
@@ -679,7 +823,11 @@ def generate(space, config: GenConfig | None = None, extents=None,
         B("  const long long qi = (long long)__float_as_int(q4.w);")
         comps = ["x", "y", "z"]
         for d in range(s):
+            if intsel:
+                B(f"  const float xq{d} = q4.{comps[d]};")
             B(f"  const double x{d} = (double)q4.{comps[d]};")
+        if intsel:
+            body.extend("  " + ln for ln in int_prelude())
         # coset-0 shift, wrapped, relative to the (approximately assigned) bin:
         # loc = k + rel lands in [0, brick) for every coset and stencil site
         rnd0 = rm0.rounding if rm0.shape == PARALLELEPIPED else ROUND_NEAREST
@@ -695,15 +843,140 @@ def generate(space, config: GenConfig | None = None, extents=None,
             B(f"  if (u{d}_ < -1) u{d}_ += {e_}; else if (u{d}_ > {bin_}) u{d}_ -= {e_};")
             B(f"  const long long rel{d} = (long long)(u{d}_ + {margin}) - kb{d};")
         ind = "  "
-    B(f"{ind}{T} acc = ({T})0;")
-    if cfg.grad:
-        for d in range(s):
-            B(f"{ind}{T} gacc{d} = ({T})0;")
+    if not sorted_:
+        B(f"{ind}{T} acc = ({T})0;")
+        if cfg.grad:
+            for d in range(s):
+                B(f"{ind}{T} gacc{d} = ({T})0;")
     em.lines = []
+    sctx = {}
 
-    def emit_coset(l, dyn):
-        """Body for coset `l` (int) or the loop variable `l` (dyn=True)."""
+    def emit_sorted_record(l, emit_u):
+        """Sorted mode, phase 1: store the (query, coset) pair's record and take its
+        rank within its psi class (warp-aggregated shared-memory counter)."""
         L = em.line
+        for d in range(s):
+            L(f"const float xf{d} = {f'xff{d}' if intsel else f'(float)xc{d}'};")
+        us = emit_u("") + ["0.0f"] * (3 - s)
+        if t.K > 1:
+            L(f"const int psi_ = {t.psi[0] if t.uniform_psi else 'sg_psi[sub]'};")
+        else:
+            L("const int psi_ = 0;")
+        L(f"sg_rec[{l * sctx['TQ']} + ql] = make_float4({us[0]}, {us[1]}, {us[2]}, "
+          f"__int_as_float(base + coff{l}));")
+        L(f"const int kp_ = valid ? psi_ : {t.K};")
+        L("const unsigned mm_ = __match_any_sync(0xffffffffu, kp_);")
+        L("const int ld_ = __ffs(mm_) - 1;")
+        L("int rb_ = 0;")
+        L(f"if ((int)lane == ld_ && kp_ < {t.K}) rb_ = atomicAdd(&sg_cnt[kp_], __popc(mm_));")
+        L("rb_ = __shfl_sync(0xffffffffu, rb_, ld_);")
+        L(f"sg_key[{l * sctx['TQ']} + ql] = valid ? ((rb_ + __popc(mm_ & lt_mask)) | (sub << 16)) : -1;")
+
+    def emit_u_factory(L):
+        """u = T_sub x_loc + t'_sub from the xf{d} (f32/f64 x_loc) in scope."""
+
+        def emit_u(tag):
+            us = []
+            if tq:
+                for d in range(3):
+                    L(f"const float4 tq{d}{tag} = *reinterpret_cast<const float4*>(&sg_Tq[sub * 12 + {4 * d}]);")
+                    name = f"u{d}{tag}"
+                    L(f"const float {name} = tq{d}{tag}.x * xf0 + tq{d}{tag}.y * xf1 + "
+                      f"tq{d}{tag}.z * xf2 + tq{d}{tag}.w;")
+                    us.append(name)
+                return us
+            for d in range(s):
+                if t.uniform_T:
+                    row = t.transforms[0][d]
+                    acc = None
+                    for e in range(s):
+                        w = row[e]
+                        if w == 0:
+                            continue
+                        term = f"xf{e}" if w == 1 else (f"(-xf{e})" if w == -1
+                                                         else f"{flit(w, fw)} * xf{e}")
+                        acc = term if acc is None else f"{acc} + {term}"
+                    acc = acc or f"({T})0"
+                else:
+                    acc = " + ".join(f"sg_T[sub * {s * s} + {d * s + e}] * xf{e}" for e in range(s))
+                if t.uniform_tp:
+                    tp = t.tshift[0][d]
+                    if tp != 0:
+                        acc = f"{acc} + {flit(tp, fw)}"
+                else:
+                    acc = f"{acc} + sg_tp[sub * {s} + {d}]"
+                name = f"u{d}{tag}"
+                L(f"const {T} {name} = {acc};")
+                us.append(name)
+            return us
+        return emit_u
+
+    def emit_int_select(l, rounding):
+        """Fixed-point rho + plane bits for coset l (assigns kk{d}, xff{d}, qq).
+
+        x = hi + lo 2^-30, o = O 2^-30.  round half away (x >= 2^-7, o <= 1/2: the value
+        x - o is never a negative tie): k = hi + ((lo - O + 2^29) >> 30),
+        x_loc = ((lo - O + 2^29) & (2^30 - 1)) - 2^29.  floor: k = hi + ((lo - O) >> 30),
+        x_loc = (lo - O) & (2^30 - 1).  Plane dots are exact int32 sums; a family's count
+        is floor(dot 2^p) = DOT >> (30 - p)."""
+        L = em.line
+        for d in range(s):
+            O = int(t.cosets[l][d] * 2 ** FIX)
+            if rounding == ROUND_NEAREST:
+                C = (1 << (FIX - 1)) - O
+                L(f"const int t{d}_ = lo{d}_ + ({C});" if C else f"const int t{d}_ = lo{d}_;")
+                L(f"kk{d} = (long long)(hi{d}_ + (t{d}_ >> 30));")
+                L(f"const int xc{d}_ = (t{d}_ & 0x3fffffff) - 0x20000000;")
+            else:
+                L(f"const int t{d}_ = lo{d}_ - ({O});" if O else f"const int t{d}_ = lo{d}_;")
+                L(f"kk{d} = (long long)(hi{d}_ + (t{d}_ >> 30));")
+                L(f"const int xc{d}_ = t{d}_ & 0x3fffffff;")
+            L(f"xff{d} = (float)xc{d}_ * 0x1p-30f;")
+        if not space.planes:
+            return
+        idots = {}
+
+        def idot(nrm):
+            if nrm not in idots:
+                terms = []
+                for e in range(s):
+                    w = int(nrm[e])
+                    if w == 0:
+                        continue
+                    terms.append((w, f"xc{e}_"))
+                expr = ""
+                for w, v in terms:
+                    mag = f"{v}" if abs(w) == 1 else f"{abs(w)} * {v}"
+                    expr += (f" + {mag}" if w > 0 else f" - {mag}") if expr else (mag if w > 0 else f"-{mag}")
+                idots[nrm] = f"di{len(idots)}_"
+                L(f"const int {idots[nrm]} = {expr or '0'};")
+            return idots[nrm]
+        done = set()
+        for i, (nrm, off) in enumerate(t.planes):
+            if nrm in families:
+                if nrm in done:
+                    continue
+                done.add(nrm)
+                b0, r, sc, m1 = families[nrm]
+                sh = FIX - (sc.bit_length() - 1)
+                dv = idot(nrm)
+                cnt = em.tmp("cnt")
+                arg = f"({dv} >> {sh}) - ({m1 - 1})" if m1 != 1 else f"{dv} >> {sh}"
+                L(f"const int {cnt} = min(max({arg}, 0), {r});")
+                L(f"qq |= ((1u << {cnt}) - 1u) << {b0};")
+                continue
+            D = int(off * 2 ** FIX)
+            L(f"qq |= ({idot(nrm)} >= {D}) ? {1 << i}u : 0u;")
+
+    def emit_coset(l, dyn, phase="all"):
+        """Body for coset `l` (int) or the loop variable `l` (dyn=True).
+
+        phase "all": selection, fetch and evaluation inline (direct / binned modes).
+        Sorted mode splits it: "select" emits the selection and stores the pair's
+        record (u, flat base index) and its rank within its psi class; "eval" emits
+        fetch + evaluation for a record whose sub, base, u0.. and psi are in scope."""
+        L = em.line if phase != "eval" else (lambda text: None)
+        dguard = "if (valid) " if phase == "select" else ""
         if dyn:
             if smem_fetch:
                 L(f"const float* V = sg_brick + l * {brick_elems};")
@@ -712,6 +985,30 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 for c in range(1, M):
                     ptr = f"(l == {c} ? (const {T}*)vol.base[{c}] : {ptr})"
                 L(f"const {T}* __restrict__ V = {ptr};")
+        else:
+            if smem_fetch:
+                L(f"const float* V = sg_brick + {l * brick_elems};")
+            else:
+                L(f"const {T}* __restrict__ V = (const {T}*)vol.base[{l}];")
+        rm = space.region_map
+        if rm.shape == PARALLELEPIPED:
+            basis, rounding = rm.basis, rm.rounding
+        else:
+            basis, rounding = exact.eye(s), ROUND_NEAREST
+        isel = intsel and not dyn and phase != "eval"
+        if isel:
+            # fast path: exact 2^-30 fixed point (int32); the fp64 path below handles the
+            # queries outside [2^-7, 2^30) (tiny, negative, huge) bit-identically
+            for d in range(s):
+                L(f"long long kk{d}; float xff{d};")
+            L("unsigned qq = 0u;")
+            L("if (fast_) {")
+            em.indent += "  "
+            emit_int_select(l, rounding)
+            em.indent = em.indent[:-2]
+            L("} else {")
+            em.indent += "  "
+        if dyn:
             for d in range(s):
                 offs = [float(t.cosets[c][d]) for c in range(M)]
                 if all(o == 0.0 for o in offs):
@@ -722,10 +1019,6 @@ def generate(space, config: GenConfig | None = None, extents=None,
                         expr = f"(l == {c} ? {dlit(t.cosets[c][d])} : {expr})"
                     L(f"const double xl{d} = __dsub_rn(x{d}, {expr});")
         else:
-            if smem_fetch:
-                L(f"const float* V = sg_brick + {l * brick_elems};")
-            else:
-                L(f"const {T}* __restrict__ V = (const {T}*)vol.base[{l}];")
             for d in range(s):
                 o = t.cosets[l][d]
                 if o == 0:
@@ -733,11 +1026,6 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 else:
                     L(f"const double xl{d} = __dsub_rn(x{d}, {dlit(o)});")
         # ---- rho (codegen.py:190-226, oracle.py:38-53)
-        rm = space.region_map
-        if rm.shape == PARALLELEPIPED:
-            basis, rounding = rm.basis, rm.rounding
-        else:
-            basis, rounding = exact.eye(s), ROUND_NEAREST
 
         def rnd(v):
             # round half away from zero == trunc(v + copysign(1/2, v)) with the same RN
@@ -770,31 +1058,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
             L("unsigned q = 0u;")
             dots = {}   # one fp64 dot product per distinct normal (planes share families)
             fam_done = set()
-            # families of parallel planes with offsets m_1..m_r * 2^-p (consecutive integers
-            # m, contiguous increasing bits): the r bits are a threshold count,
-            # cnt = clamp(floor(dot * 2^p) - m_1 + 1, 0, r) -- exact, because dot * 2^p is
-            # exact and comparing with integers commutes with floor
-            fams = {}
-            for i, (nrm, off) in enumerate(t.planes):
-                fams.setdefault(nrm, []).append((i, off))
-            counted = {}
-            for nrm, lst in fams.items():
-                if len(lst) < 3:
-                    continue
-                idxs = [i for i, _ in lst]
-                offs = [o for _, o in lst]
-                if idxs != list(range(idxs[0], idxs[0] + len(idxs))):
-                    continue
-                step = offs[1] - offs[0]
-                if step <= 0 or any(offs[k + 1] - offs[k] != step for k in range(len(offs) - 1)):
-                    continue
-                inv = 1 / step
-                if inv.denominator != 1 or int(inv) & (int(inv) - 1):
-                    continue   # spacing must be 2^-p so the scaling is exact
-                m1 = offs[0] * inv
-                if m1.denominator != 1:
-                    continue
-                counted[nrm] = (idxs[0], len(idxs), int(inv), int(m1))
+            counted = families
             for i, (nrm, off) in enumerate(t.planes):
                 if nrm in counted:
                     if nrm in fam_done:
@@ -834,6 +1098,18 @@ def generate(space, config: GenConfig | None = None, extents=None,
                     dots[nrm] = f"dn{len(dots)}"
                     L(f"const double {dots[nrm]} = {acc or '0.0'};")
                 L(f"q |= ({dots[nrm]} >= {dlit(off)}) ? {1 << i}u : 0u;")
+        if isel:
+            for d in range(s):
+                L(f"kk{d} = k{d}; xff{d} = (float)xc{d};")
+            if space.planes:
+                L("qq = q;")
+            em.indent = em.indent[:-2]
+            L("}")
+            for d in range(s):
+                L(f"const long long k{d} = kk{d};")
+            if space.planes:
+                L("unsigned q = qq;")
+        if space.planes:
             if t.compress:
                 L(f"q = q % {P}u;")
             if sigma_global:
@@ -843,8 +1119,6 @@ def generate(space, config: GenConfig | None = None, extents=None,
             else:
                 v = t.sigma[0] if t.sigma else 0
                 L(f"int sub = {v};")
-                if any(x < 0 for x in t.sigma):
-                    pass
             if any(x < 0 for x in t.sigma):
                 if use_sigma:
                     L("if (sub < 0) { atomicOr(err, 1u); sub = 0; }")
@@ -858,8 +1132,8 @@ def generate(space, config: GenConfig | None = None, extents=None,
             cols = s + 1
             base = f"(qi * {M} + {l}) * {cols}" if not dyn else f"(qi * {M} + l) * {cols}"
             for d in range(s):
-                L(f"dbg[{base} + {d}] = (int)k{d};")
-            L(f"dbg[{base} + {s}] = sub;")
+                L(f"{dguard}dbg[{base} + {d}] = (int)k{d};")
+            L(f"{dguard}dbg[{base} + {s}] = sub;")
         # ---- wrap k once per coset, flat base index in the padded array
         geo = 0 if (same_geom or dyn) else l
         if not same_geom and dyn:
@@ -876,6 +1150,10 @@ def generate(space, config: GenConfig | None = None, extents=None,
                   f"kw{d} = (int)(m_ < 0 ? m_ + {e_[d]}LL : m_); }}")
         L("const int base = " + " + ".join(
             f"kw{d} * {st_[d]}" if st_[d] != 1 else f"kw{d}" for d in range(s)) + ";")
+        if phase == "select":
+            emit_sorted_record(l, emit_u_factory(L))
+            return
+        L = em.line
         # ---- per-sub fetch offsets
         if fetch_mode == "affine":
             gi = 0 if same_geom else geo
@@ -919,46 +1197,17 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 o = sum(sten[j][d] * st_[d] for d in range(s))
                 return f"base + ({o})" if o else "base"
         # ---- local point u = T x_loc + t'
-        for d in range(s):
-            L(f"const {T} xf{d} = ({T})xc{d};")
+        if phase == "all":
+            for d in range(s):
+                L(f"const {T} xf{d} = {f'xff{d}' if (intsel and not dyn) else f'({T})xc{d}'};")
 
         def emit_u(tag):
-            us = []
-            if tq:
-                for d in range(3):
-                    L(f"const float4 tq{d}{tag} = *reinterpret_cast<const float4*>(&sg_Tq[sub * 12 + {4 * d}]);")
-                    name = f"u{d}{tag}"
-                    L(f"const float {name} = tq{d}{tag}.x * xf0 + tq{d}{tag}.y * xf1 + "
-                      f"tq{d}{tag}.z * xf2 + tq{d}{tag}.w;")
-                    us.append(name)
-                return us
-            for d in range(s):
-                if t.uniform_T:
-                    row = t.transforms[0][d]
-                    acc = None
-                    for e in range(s):
-                        w = row[e]
-                        if w == 0:
-                            continue
-                        term = f"xf{e}" if w == 1 else (f"(-xf{e})" if w == -1
-                                                         else f"{flit(w, fw)} * xf{e}")
-                        acc = term if acc is None else f"{acc} + {term}"
-                    acc = acc or f"({T})0"
-                else:
-                    acc = " + ".join(f"sg_T[sub * {s * s} + {d * s + e}] * xf{e}" for e in range(s))
-                if t.uniform_tp:
-                    tp = t.tshift[0][d]
-                    if tp != 0:
-                        acc = f"{acc} + {flit(tp, fw)}"
-                else:
-                    acc = f"{acc} + sg_tp[sub * {s} + {d}]"
-                name = f"u{d}{tag}"
-                L(f"const {T} {name} = {acc};")
-                us.append(name)
-            return us
+            if phase == "eval":
+                return [f"u{d}" for d in range(s)]     # loaded from the pair's record
+            return emit_u_factory(L)(tag)
 
         # ---- fetch + compute following the (m, d) plan
-        if t.K > 1:
+        if t.K > 1 and phase != "eval":
             if t.uniform_psi:
                 L(f"const int psi = {t.psi[0]};")
             else:
@@ -1163,6 +1412,19 @@ def generate(space, config: GenConfig | None = None, extents=None,
 
         if cfg.coeffs == "table":
             run_table()
+        elif phase == "eval" and t.K > 1:
+            # pairs are sorted by psi: every warp but the class-boundary ones takes one arm
+            L("switch (psi) {")
+            for i in range(t.K):
+                L(f"{'default' if i == t.K - 1 else f'case {i}'}: {{")
+                em.indent += "  "
+                accs, grads, _ = run_plan([i], f"_{i}")
+                L(f"acc += {accs[i]};")
+                if cfg.grad:
+                    add_grad(grads[i], True)
+                em.indent = em.indent[:-2]
+                L("} break;")
+            L("}")
         elif t.K == 1:
             accs, grads, _ = run_plan([0], "")
             L(f"acc += {accs[0]};")
@@ -1192,7 +1454,104 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 em.indent = em.indent[:-2]
             L("}")
 
-    if M == 1:
+    if sorted_:
+        TQ, Bk = cfg.tile, cfg.block
+        PQ = TQ // Bk
+        sctx["TQ"] = TQ
+        for r in range(PQ):
+            body.append(f"    {{  // query {r} of this thread in the tile")
+            body.append(f"    const int ql = {r * Bk} + (int)threadIdx.x;")
+            body.append("    const long long qi = q0 + ql;")
+            body.append("    const bool valid = qi < n;")
+            body.append("    const long long qc = valid ? qi : n - 1;")
+            for d in range(s):
+                if intsel:
+                    body.append(f"    const float xq{d} = xs[qc * {s} + {d}];")
+                    body.append(f"    const double x{d} = (double)xq{d};")
+                else:
+                    body.append(f"    const double x{d} = (double)xs[qc * {s} + {d}];")
+            if intsel:
+                body.extend("    " + ln for ln in int_prelude())
+            sctx["r"] = r
+            for l in range(M):
+                em.lines = []
+                em.indent = "      "
+                em.line(f"{{  // coset {l}")
+                em.indent = "        "
+                emit_coset(l, False, phase="select")
+                em.indent = "      "
+                em.line("}")
+                body.extend(em.lines)
+            body.append("    }")
+        body.append("    __syncthreads();")
+        # exclusive scan of the per-psi counts (K <= 32), counters reset for the next tile
+        body.append("    if (threadIdx.x < 32) {")
+        body.append(f"      const int c_ = (int)lane < {t.K} ? sg_cnt[lane] : 0;")
+        body.append("      int v_ = c_;")
+        body.append("      for (int o_ = 1; o_ < 32; o_ <<= 1) { const int w_ = __shfl_up_sync(0xffffffffu, v_, o_); if ((int)lane >= o_) v_ += w_; }")
+        body.append("      sg_start[lane] = v_ - c_;")
+        body.append("      if (lane == 31) sg_tot = v_;")
+        body.append("      sg_cnt[lane] = 0;")
+        body.append("    }")
+        body.append("    __syncthreads();")
+        psi_of = (lambda sub: str(t.psi[0])) if (t.K == 1 or t.uniform_psi) else (lambda sub: f"sg_psi[{sub}]")
+        if t.K == 1:
+            psi_of = lambda sub: "0"   # noqa: E731
+        body.append(f"    for (int i_ = threadIdx.x; i_ < {M * TQ}; i_ += {Bk}) {{")
+        body.append("      const int k_ = sg_key[i_];")
+        body.append("      if (k_ >= 0) { const int sb_ = k_ >> 16; "
+                    f"sg_ord[sg_start[{psi_of('sb_')}] + (k_ & 0xffff)] = i_ | (sb_ << 16); }}")
+        body.append("    }")
+        body.append("    __syncthreads();")
+        # phase 2: evaluate the pairs in psi order
+        body.append("    const int tot = sg_tot;")
+        body.append(f"    for (int pos = threadIdx.x; pos < tot; pos += {Bk}) {{")
+        body.append("      const int e_ = sg_ord[pos];")
+        body.append("      const int pi_ = e_ & 0xffff;")
+        body.append("      const int sub = e_ >> 16;")
+        body.append("      const float4 rec = sg_rec[pi_];")
+        for d in range(s):
+            body.append(f"      const float u{d} = rec.{'xyz'[d]};")
+        body.append("      const int base = __float_as_int(rec.w);")
+        body.append(f"      const float* __restrict__ V = (const float*)vol.base[0];")
+        if t.K > 1:
+            body.append(f"      const int psi = {psi_of('sub')};")
+        body.append("      float acc = 0.0f;")
+        if cfg.grad:
+            for d in range(s):
+                body.append(f"      float gacc{d} = 0.0f;")
+        em.lines = []
+        em.indent = "      "
+        emit_coset(0, False, phase="eval")
+        body.extend(em.lines)
+        if cfg.grad:
+            g = ", ".join([f"gacc{d}" for d in range(s)] + ["0.0f"] * (3 - s))
+            body.append(f"      sg_res4[pi_] = make_float4(acc, {g});")
+        else:
+            body.append("      sg_res[pi_] = acc;")
+        body.append("    }")
+        body.append("    __syncthreads();")
+        # phase 3: coset contributions summed in coset order, coalesced stores
+        body.append(f"    for (int ql = threadIdx.x; ql < {TQ}; ql += {Bk}) {{")
+        body.append("      const long long qi = q0 + ql;")
+        body.append("      if (qi >= n) break;")
+        if cfg.grad:
+            body.append("      float4 a_ = sg_res4[ql];")
+            for l in range(1, M):
+                body.append(f"      {{ const float4 b_ = sg_res4[{l * TQ} + ql]; a_.x += b_.x; a_.y += b_.y; a_.z += b_.z; a_.w += b_.w; }}")
+            body.append("      out[qi] = a_.x;")
+            for d in range(s):
+                body.append(f"      grad[qi * {s} + {d}] = a_.{'yzw'[d]};")
+        else:
+            expr = "sg_res[ql]"
+            for l in range(1, M):
+                expr = f"({expr} + sg_res[{l * TQ} + ql])"
+            body.append(f"      out[qi] = 0.0f + {expr};")
+        body.append("    }")
+        body.append("    __syncthreads();")
+        body.append("  }")   # tile loop
+        body.append("}")
+    elif M == 1:
         em.line("{")
         em.indent = "    "
         emit_coset(0, False)
@@ -1212,13 +1571,14 @@ def generate(space, config: GenConfig | None = None, extents=None,
         emit_coset(None, True)
         em.indent = "  "
         em.line("}")
-    body += em.lines
-    body.append("  out[qi] = acc;")
-    if cfg.grad:
-        for d in range(s):
-            body.append(f"  grad[qi * {s} + {d}] = gacc{d};")
-    body.append("  }")   # query loop (grid-stride in direct mode, chunk loop in binned mode)
-    body.append("}")
+    if not sorted_:
+        body += em.lines
+        body.append("  out[qi] = acc;")
+        if cfg.grad:
+            for d in range(s):
+                body.append(f"  grad[qi * {s} + {d}] = gacc{d};")
+        body.append("  }")   # query loop (grid-stride in direct mode, chunk loop in binned mode)
+        body.append("}")
     if lut:
         lit = ", ".join(flit(Fraction(v), fw) for v in lut)
         head.append(f"__constant__ {T} sg_lut[{len(lut)}] = {{{lit}}};")
@@ -1228,8 +1588,10 @@ def generate(space, config: GenConfig | None = None, extents=None,
         block=cfg.block, halo=H, extents=ext, padded_extents=pext, has_grad=cfg.grad,
         has_dbg=cfg.dbg, config=cfg, space=space,
         mode=cfg.mode, bin=bin_ if binned else 0, brick=tuple(brick) if binned else (),
-        smem_bytes=smem_bytes if binned else 0, stage_tma=binned and cfg.stage == "tma",
+        smem_bytes=smem_bytes if binned else (sorted_smem if sorted_ else 0),
+        stage_tma=binned and cfg.stage == "tma",
         chunk=cfg.chunk if binned else 0,
+        queries_per_thread=cfg.tile // cfg.block if sorted_ else 1,
         rounding=(0 if (rm0.shape == PARALLELEPIPED and rm0.rounding == "floor") else 1),
         meta={"fetch_mode": fetch_mode, "K": t.K, "nsub": t.nsub, "n": t.n, "reach": h,
               "smem_tables": [x[0] for x in smem], "lut_entries": len(lut)})

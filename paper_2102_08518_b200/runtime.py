@@ -181,7 +181,7 @@ class Module:
         info.has_grad = int(prog.has_grad)
         info.has_dbg = int(prog.has_dbg)
         info.halo = prog.halo
-        info.queries_per_thread = 1
+        info.queries_per_thread = getattr(prog, "queries_per_thread", 1)
         for c, row in enumerate(prog.padded_extents):
             for d, e in enumerate(row):
                 info.padded_extents[c][d] = e

@@ -37,10 +37,13 @@ def _xs(z, which, dtype=torch.float32):
 
 
 @pytest.mark.parametrize("name", golden_names())
-@pytest.mark.parametrize("mode", ["direct", "binned"])
+@pytest.mark.parametrize("mode", ["direct", "binned", "sorted", "direct_f64"])
 def test_selection_bit_exact(name, mode):
     space, _, z, arrays = load_golden(name)
-    ev = _evaluator(space, arrays, dbg=True, mode=mode)
+    if mode == "direct_f64":
+        ev = _evaluator(space, arrays, dbg=True, select="f64")
+    else:
+        ev = _evaluator(space, arrays, dbg=True, mode=mode)
     for which in SETS:
         out, _, dbg = ev(_xs(z, which))
         dbg = dbg.cpu().numpy()
@@ -68,6 +71,13 @@ CONFIGS = [
     dict(coeffs="table", mode="binned", params_md=(2, 4)),
     dict(form="sym"),
     dict(form="sym", mode="binned", params_mode="branchy"),
+    dict(mode="sorted"),
+    dict(select="f64"),
+    dict(select="f64", mode="binned"),
+    dict(select="f64", mode="sorted", form="sym"),
+    dict(mode="sorted", form="sym", block=256, tile=512),
+    dict(mode="sorted", coeffs="table", tile=256),
+    dict(mode="sorted", params_md=(2, 4), form="sites"),
 ]
 
 
@@ -108,7 +118,7 @@ def test_values_f64_variant(name):
 
 
 @pytest.mark.parametrize("name", golden_names())
-@pytest.mark.parametrize("mode", ["direct", "binned", "table", "sym"])
+@pytest.mark.parametrize("mode", ["direct", "binned", "table", "sym", "sorted", "sorted_sym"])
 def test_gradient_vs_oracle(name, mode):
     space, ospace, z, arrays = load_golden(name)
     xs = z["uniform_xs"].astype(np.float64)
@@ -118,6 +128,8 @@ def test_gradient_vs_oracle(name, mode):
         ev = _evaluator(space, arrays, grad=True, coeffs="table")
     elif mode == "sym":
         ev = _evaluator(space, arrays, grad=True, form="sym")
+    elif mode == "sorted_sym":
+        ev = _evaluator(space, arrays, grad=True, form="sym", mode="sorted", block=256)
     else:
         ev = _evaluator(space, arrays, grad=True, mode=mode)
     out, g, _ = ev(_xs(z, "uniform"))
@@ -127,7 +139,7 @@ def test_gradient_vs_oracle(name, mode):
 
 
 @pytest.mark.parametrize("name", golden_names())
-@pytest.mark.parametrize("mode", ["direct", "binned"])
+@pytest.mark.parametrize("mode", ["direct", "binned", "sorted"])
 def test_host_path_matches_device_path(name, mode):
     space, _, z, arrays = load_golden(name)
     ev = _evaluator(space, arrays, mode=mode)

@@ -26,6 +26,13 @@ VARIANTS = {
     "imm_pred": dict(coeffs="imm"),
     "direct": dict(mode="direct", block=128),
     "sym": dict(form="sym"),
+    "f64sel": dict(select="f64"),
+    "sorted": dict(mode="sorted", block=256),
+    "sorted_sym": dict(mode="sorted", form="sym", block=256),
+    "sorted_b128": dict(mode="sorted", block=128),
+    "sorted_b512": dict(mode="sorted", block=512),
+    "sorted_t1024": dict(mode="sorted", block=256, tile=1024),
+    "sorted_table": dict(mode="sorted", block=256, coeffs="table"),
 }
 
 
