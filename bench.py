@@ -13,6 +13,10 @@ of the results, every step).
 Configs (BASELINE.json, restated concretely in SURVEY.md 8d):
   c1  tricubic B-spline on Z^3, 64^3, 2^20 uniform queries
   c2  BCC quintic box spline, 2 x 101^3 coset-split, 2^24 uniform queries  (default)
+  c3  BCC Voronoi spline (order 2), 2 x 203^3, 2^26 ray-ordered queries
+  c4  FCC 6-direction box spline, 4 x 161^3, 2^26 uniform queries, value + gradient
+  c4v FCC Voronoi spline (order 2), 4 x 161^3, 2^26 uniform queries, value + gradient
+  c5  BCC Voronoi spline, 2 x 406^3, 2^30 ray-ordered queries (strong-scaled over the GPUs)
 Under torchrun every rank evaluates its own batch (weak scaling, volume replicated).
 """
 
@@ -47,11 +51,14 @@ CONFIGS = {
                desc="BCC quintic box spline (4 dirs x2), 2x101^3 coset-split, 2^24 uniform"),
     "c3": dict(space="bcc_voronoi2", extents=(203, 203, 203), queries=1 << 26, kind="rays",
                rays=(512, 512, 256), grad=False, scaling="weak",
-               variant=dict(mode="direct", coeffs="imm", block=128),
+               variant=dict(mode="sorted", coeffs="imm", block=512),
                desc="BCC Voronoi spline (order 2, piecewise cubic), 2x203^3, 2^26 ray-ordered"),
     "c4": dict(space="fcc_box6", extents=(161, 161, 161), queries=1 << 26, kind="uniform",
                grad=True, scaling="weak", variant=dict(mode="direct", coeffs="imm", block=128),
                desc="FCC 6-direction box spline, 4x161^3, 2^26 uniform, value + gradient"),
+    "c4v": dict(space="fcc_voronoi2", extents=(161, 161, 161), queries=1 << 26, kind="uniform",
+                grad=True, scaling="weak", variant=dict(mode="direct", coeffs="table", block=128),
+                desc="FCC Voronoi spline (order 2), 4x161^3, 2^26 uniform, value + gradient"),
     "c5": dict(space="bcc_voronoi2", extents=(406, 406, 406), queries=1 << 30, kind="rays",
                rays=(1024, 1024, 1024), grad=False, scaling="strong",
                variant=dict(mode="direct", coeffs="imm", block=128),

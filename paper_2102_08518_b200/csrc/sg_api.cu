@@ -642,6 +642,7 @@ int sg_module_load(const void* image, size_t image_len, const char* entry, int d
       if (e != cudaSuccess) {
         cudaLibraryUnload(m->lib);
         delete m;
+        cudaGetLastError();   // clear the non-sticky error so later calls do not report it
         return fail(SG_ECUDA, "smem attribute: %s", cudaGetErrorString(e));
       }
     }
@@ -653,6 +654,7 @@ int sg_module_load(const void* image, size_t image_len, const char* entry, int d
     if (e != cudaSuccess) {
       cudaLibraryUnload(m->lib);
       delete m;
+      cudaGetLastError();
       return fail(SG_ECUDA, "smem attribute: %s", cudaGetErrorString(e));
     }
   }

@@ -66,6 +66,7 @@ class GenConfig:
     stage: str = "tma"           # binned: brick staging, "tma" (cp.async.bulk.tensor) | "ldg"
     tile: int = 0                # sorted: queries per CTA tile (0 = auto: 2 CTAs / SM of smem)
     select: str = "auto"         # selection arithmetic: "f64" | "int" (2^-30 fixed point) | "auto"
+    sigma_smem: int = 4096       # sigma tables up to this many entries are staged in smem
 
     def __post_init__(self):
         if self.float_width not in (F64, F32):
@@ -385,11 +386,15 @@ class CudaProgram:
         return np.float32 if self.float_width == F32 else np.float64
 
 
+def _sigma_short(t: Tables) -> bool:
+    return all(-32768 <= v < 32768 for v in t.sigma)
+
+
 def _table_bytes(space, t: Tables, cfg) -> int:
     """Upper estimate of the per-CTA shared-memory tables (sigma, transforms, offsets, LUT)."""
     b = 0
-    if len(t.sigma) <= 4096:
-        b += 4 * len(t.sigma)
+    if len(t.sigma) <= cfg.sigma_smem:
+        b += (2 if _sigma_short(t) else 4) * len(t.sigma)
     b += 4 * 12 * t.nsub            # transforms + t'
     b += 4 * (t.n + 1) * t.nsub     # stencil offsets (table mode)
     b += 4 * t.nsub                 # psi
@@ -590,9 +595,9 @@ def generate(space, config: GenConfig | None = None, extents=None,
     # ---- tables ------------------------------------------------------------
     smem = []     # (name, ctype, values)
     use_sigma = t.nsub > 1 and len(space.planes) > 0 and len(set(t.sigma)) > 1
-    sigma_global = use_sigma and len(t.sigma) > 4096
+    sigma_global = use_sigma and len(t.sigma) > cfg.sigma_smem
     if use_sigma and not sigma_global:
-        smem.append(("sg_sigma", "int", list(t.sigma)))
+        smem.append(("sg_sigma", "short" if _sigma_short(t) else "int", list(t.sigma)))
     tq = s == 3 and fw == F32 and not (t.uniform_T and t.uniform_tp)
     if tq:
         # rows (T[d][0], T[d][1], T[d][2], t'[d]) per sub-region: 3 LDS.128 per coset
@@ -669,7 +674,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
         consts = None
 
     for name, ctype, vals in smem:
-        lit = ", ".join(repr(v) if ctype != "int" else str(v) for v in vals)
+        lit = ", ".join(repr(v) if ctype not in ("int", "short") else str(v) for v in vals)
         if ctype == "float":
             lit = ", ".join(flit(Fraction(v), F32) for v in vals)
         elif ctype == "double":
@@ -682,9 +687,11 @@ def generate(space, config: GenConfig | None = None, extents=None,
     # ---- kernel -------------------------------------------------------------
     def int_prelude():
         """Per query: fixed-point split x = hi + lo * 2^-30 (lo in [0, 2^30)), exact for the
-        fast-path range 2^-7 <= x < 2^30; other queries take the fp64 path."""
+        fast-path range 2^-7 <= x < E (so 0 <= k <= E: one conditional subtract wraps it);
+        other queries take the fp64 path."""
+        emin = [min(e[d] for e in ext) for d in range(s)]
         out = ["const bool fast_ = " + " && ".join(
-            f"(xq{d} >= 0x1p-7f) && (xq{d} < 0x1p+30f)" for d in range(s)) + ";"]
+            f"(xq{d} >= 0x1p-7f) && (xq{d} < {float(emin[d])!r}f)" for d in range(s)) + ";"]
         for d in range(s):
             out.append(f"const long long X{d}_ = __float2ll_rn(xq{d} * 0x1p+30f);")
             out.append(f"const int hi{d}_ = (int)(X{d}_ >> 30);")
@@ -911,7 +918,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
             return us
         return emit_u
 
-    def emit_int_select(l, rounding):
+    def emit_int_select(l, rounding, wrap_ext=None):
         """Fixed-point rho + plane bits for coset l (assigns kk{d}, xff{d}, qq).
 
         x = hi + lo 2^-30, o = O 2^-30.  round half away (x >= 2^-7, o <= 1/2: the value
@@ -925,11 +932,17 @@ def generate(space, config: GenConfig | None = None, extents=None,
             if rounding == ROUND_NEAREST:
                 C = (1 << (FIX - 1)) - O
                 L(f"const int t{d}_ = lo{d}_ + ({C});" if C else f"const int t{d}_ = lo{d}_;")
-                L(f"kk{d} = (long long)(hi{d}_ + (t{d}_ >> 30));")
+                L(f"const int k{d}_ = hi{d}_ + (t{d}_ >> 30);")
+                L(f"kk{d} = (long long)k{d}_;")
+                if wrap_ext:
+                    L(f"kwv{d} = k{d}_ >= {wrap_ext[d]} ? k{d}_ - {wrap_ext[d]} : k{d}_;")
                 L(f"const int xc{d}_ = (t{d}_ & 0x3fffffff) - 0x20000000;")
             else:
                 L(f"const int t{d}_ = lo{d}_ - ({O});" if O else f"const int t{d}_ = lo{d}_;")
-                L(f"kk{d} = (long long)(hi{d}_ + (t{d}_ >> 30));")
+                L(f"const int k{d}_ = hi{d}_ + (t{d}_ >> 30);")
+                L(f"kk{d} = (long long)k{d}_;")
+                if wrap_ext:
+                    L(f"kwv{d} = k{d}_ < 0 ? k{d}_ + {wrap_ext[d]} : k{d}_;")
                 L(f"const int xc{d}_ = t{d}_ & 0x3fffffff;")
             L(f"xff{d} = (float)xc{d}_ * 0x1p-30f;")
         if not space.planes:
@@ -996,15 +1009,16 @@ def generate(space, config: GenConfig | None = None, extents=None,
         else:
             basis, rounding = exact.eye(s), ROUND_NEAREST
         isel = intsel and not dyn and phase != "eval"
+        wrap_ext = list(ext[0 if same_geom else l]) if (isel and not smem_fetch) else None
         if isel:
             # fast path: exact 2^-30 fixed point (int32); the fp64 path below handles the
-            # queries outside [2^-7, 2^30) (tiny, negative, huge) bit-identically
+            # queries outside [2^-7, E) (tiny, negative, beyond the box) bit-identically
             for d in range(s):
-                L(f"long long kk{d}; float xff{d};")
+                L(f"long long kk{d}; float xff{d};" + (f" int kwv{d};" if wrap_ext else ""))
             L("unsigned qq = 0u;")
             L("if (fast_) {")
             em.indent += "  "
-            emit_int_select(l, rounding)
+            emit_int_select(l, rounding, wrap_ext)
             em.indent = em.indent[:-2]
             L("} else {")
             em.indent += "  "
@@ -1101,6 +1115,10 @@ def generate(space, config: GenConfig | None = None, extents=None,
         if isel:
             for d in range(s):
                 L(f"kk{d} = k{d}; xff{d} = (float)xc{d};")
+                if wrap_ext:
+                    L(f"kwv{d} = (int)k{d};")
+                    L(f"if ((unsigned)kwv{d} >= {wrap_ext[d]}u) {{ long long m_ = k{d} % {wrap_ext[d]}LL; "
+                      f"kwv{d} = (int)(m_ < 0 ? m_ + {wrap_ext[d]}LL : m_); }}")
             if space.planes:
                 L("qq = q;")
             em.indent = em.indent[:-2]
@@ -1143,6 +1161,9 @@ def generate(space, config: GenConfig | None = None, extents=None,
         if smem_fetch:
             for d in range(s):
                 L(f"const int kw{d} = (int)(k{d} + rel{d});")
+        elif wrap_ext:
+            for d in range(s):
+                L(f"const int kw{d} = kwv{d};")
         else:
             for d in range(s):
                 L(f"int kw{d} = (int)k{d};")

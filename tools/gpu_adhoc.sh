@@ -1,7 +1,4 @@
 mkdir -p gpurun_out
-python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -2
-for cv in "c3 default" "c3 sorted_b512" "c4 sorted_b512" "c2 default"; do
-  set -- $cv
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:sg_eval_kernel -s 1 -c 1 -o gpurun_out/prof_$1_$2_int -f python tools/variants.py $1 --only $2 --reps 1 > /dev/null 2>&1
-done
-ls -la gpurun_out/*.ncu-rep
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" 2>&1 | tail -2
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -4
+echo "== variants c4v"; timeout 600 python tools/variants.py c4v --reps 10 2>&1 | grep -E "Grecon|FAIL|Error"

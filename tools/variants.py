@@ -33,6 +33,11 @@ VARIANTS = {
     "sorted_b512": dict(mode="sorted", block=512),
     "sorted_t1024": dict(mode="sorted", block=256, tile=1024),
     "sorted_table": dict(mode="sorted", block=256, coeffs="table"),
+    "sorted_b512_sglobal": dict(mode="sorted", block=512, sigma_smem=0),
+    "sorted_b1024": dict(mode="sorted", block=1024),
+    "sorted_b512_t1536": dict(mode="sorted", block=512, tile=1536),
+    "sorted_b512_t2048": dict(mode="sorted", block=512, tile=2048),
+    "sglobal": dict(sigma_smem=0),
 }
 
 
