@@ -278,6 +278,45 @@ def make_inputs(cfg_name, rank, device, world=1):
     return space, arrays, xs
 
 
+def roofline(cfg_name, falg, n, eval_kernel_ms, step_ms, pk):
+    """roofline block of the bench line for the dominant kernel (sg_eval_kernel).
+
+    achieved = algorithmic FP32 work (the reference's own dynamic op count F_alg per query,
+    SURVEY 8d) x queries / the kernel's CUDA-event time; peak = FP32 FMA peak.  The
+    kernel may execute fewer flops than F_alg (symmetry-rewritten / factored forms), so
+    `executed` restates the same time against the FP32 flops the kernel actually ran and
+    `issue` against the SM issue rate (4 warp-instructions / clk / SM) -- both counted by
+    ncu on the same launch (profiles/ncu_<config>.json)."""
+    if not falg:
+        return None
+    achieved = falg * n / (eval_kernel_ms / 1e3) / 1e12
+    roof = {"bound": "fp32", "achieved": round(achieved, 3), "peak": round(pk["fp32_tflops"], 2),
+            "unit": "TFLOP/s", "frac": round(achieved / pk["fp32_tflops"], 4), "traffic": None,
+            "note": f"F_alg = {falg:g} FP ops/query (reference dynamic count, m=1 d=n branchy; "
+                    f"tests/golden/falg.json) x {n} queries / sg_eval_kernel time "
+                    f"({eval_kernel_ms:.4f} ms of the {step_ms:.4f} ms step, CUDA events on the "
+                    f"launch stream); peak = 148 SM x 128 FP32 lanes x 2 x {pk['sm_max_mhz']:.0f} MHz "
+                    f"({pk['source']} sm_max_mhz)"}
+    prof = PROFILES / f"ncu_{cfg_name}.json"
+    if prof.exists():
+        d = json.loads(prof.read_text())
+        roof["traffic"] = d.get("dram_bytes_per_launch")
+        ex = d.get("executed_fp32_flops_per_query")
+        if ex:
+            a = ex * n / (eval_kernel_ms / 1e3) / 1e12
+            roof["executed"] = {"flops_per_query": round(ex, 1), "achieved": round(a, 3),
+                                "frac": round(a / pk["fp32_tflops"], 4), "unit": "TFLOP/s"}
+        wi = d.get("warp_inst_per_query")
+        if wi:
+            peak_gi = 148 * 4 * pk["sm_max_mhz"] / 1e3          # G warp-instructions / s
+            a = wi * n / (eval_kernel_ms / 1e3) / 1e9
+            roof["issue"] = {"warp_inst_per_query": round(wi, 2), "achieved": round(a, 1),
+                             "peak": round(peak_gi, 1), "unit": "Gwarp-inst/s",
+                             "frac": round(a / peak_gi, 4)}
+        roof["profile"] = f"profiles/ncu_{cfg_name}.json ({d.get('source', '')})"
+    return roof
+
+
 def run_ours(args, rank, world, device):
     import torch
     import torch.distributed as dist
@@ -376,21 +415,7 @@ def run_ours(args, rank, world, device):
         return None
     pk = peaks()
     falg = falg_per_query(c["space"])
-    roof = None
-    if falg:
-        achieved = falg * n / (eval_kernel_ms / 1e3) / 1e12
-        traffic = None
-        tp = PROFILES / f"traffic_{args.config}.json"
-        if tp.exists():
-            traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
-        roof = {"bound": "fp32", "achieved": round(achieved, 3), "peak": round(pk["fp32_tflops"], 2),
-                "unit": "TFLOP/s", "frac": round(achieved / pk["fp32_tflops"], 4),
-                "traffic": traffic,
-                "note": f"F_alg = {falg:g} FP ops/query (reference dynamic count, m=1 d=n branchy; "
-                        f"tests/golden/falg.json); peak = 148 SM x 128 FP32 lanes x 2 x "
-                        f"{pk['sm_max_mhz']:.0f} MHz ({pk['source']} sm_max_mhz); dominant kernel "
-                        f"sg_eval_kernel timed with CUDA events on the launch stream: "
-                        f"{eval_kernel_ms:.4f} ms of the {kernel_ms:.4f} ms step (rest: query binning)"}
+    roof = roofline(args.config, falg, n, eval_kernel_ms, kernel_ms, pk)
     line = {
         "metric": "G reconstructions/sec per B200 (fraction of FP32 roofline in roofline)",
         "value": round(value, 4), "unit": "Grecon/s", "n_gpus": world, "steps": args.steps,

@@ -65,6 +65,7 @@ class GenConfig:
     brick_budget: int = 112 * 1024   # binned auto-bin: shared-memory budget for the bricks
     stage: str = "tma"           # binned: brick staging, "tma" (cp.async.bulk.tensor) | "ldg"
     tile: int = 0                # sorted: queries per CTA tile (0 = auto: 2 CTAs / SM of smem)
+    stream: str = "cs"           # query/result cache policy: "cs" (evict-first) | "default"
     select: str = "auto"         # selection arithmetic: "f64" | "int" (2^-30 fixed point) | "auto"
     sigma_smem: int = 4096       # sigma tables up to this many entries are staged in smem
 
@@ -79,6 +80,8 @@ class GenConfig:
             raise ValueError("block must be a multiple of 32 in [32, 1024]")
         if self.mode not in ("direct", "binned", "sorted"):
             raise ValueError("mode must be 'direct', 'binned' or 'sorted'")
+        if self.stream not in ("cs", "default"):
+            raise ValueError("stream must be 'cs' or 'default'")
         if self.select not in ("auto", "f64", "int"):
             raise ValueError("select must be 'auto', 'f64' or 'int'")
         if self.mode == "sorted" and (self.tile % self.block or self.tile > 8192 or self.tile < 0):
@@ -548,6 +551,9 @@ def generate(space, config: GenConfig | None = None, extents=None,
         smem_bytes = 0
 
     fw = cfg.float_width
+    # query / result streams: evict-first (streaming) so they do not push the coefficient
+    # volume out of L2; plain __ldg / stores with stream="default"
+    ldf, stf = ("__ldcs", "__stcs") if cfg.stream == "cs" else ("__ldg", "sg_st")
     intsel = cfg.select != "f64" and (M == 1 or cfg.unroll_cosets) and int_selection_ok(space, t, fw)
     if cfg.select == "int" and not intsel:
         raise ValueError("this space/variant cannot use the integer selection path")
@@ -588,6 +594,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
     A(f"// extents={ext} stencil reach={h} padded={pext[0]} halo={H} mode={cfg.mode}"
       + (f" bin={bin_} brick={tuple(brick)} stage={cfg.stage}" if binned else ""))
     A("struct SgCosets { const void* base[8]; };")
+    A("template <typename T> __device__ __forceinline__ void sg_st(T* p, T v) { *p = v; }")
     if binned:
         A("struct __align__(64) SgTmap { unsigned long long opaque[16]; };")
         A("struct SgTmaps { SgTmap m[8]; };")
@@ -747,10 +754,10 @@ def generate(space, config: GenConfig | None = None, extents=None,
           B(f"       qi += (long long)gridDim.x * {cfg.block}) {{")
           for d in range(s):
               if intsel:
-                  B(f"  const float xq{d} = xs[qi * {s} + {d}];")
+                  B(f"  const float xq{d} = {ldf}(&xs[qi * {s} + {d}]);")
                   B(f"  const double x{d} = (double)xq{d};")
               else:
-                  B(f"  const double x{d} = (double)xs[qi * {s} + {d}];")
+                  B(f"  const double x{d} = (double){ldf}(&xs[qi * {s} + {d}]);")
           if intsel:
               body.extend("  " + ln for ln in int_prelude())
           ind = "  "
@@ -823,10 +830,10 @@ def generate(space, config: GenConfig | None = None, extents=None,
             B('  asm volatile("{\\n .reg .pred p;\\n SG_WAIT_%=:\\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\\n @!p bra SG_WAIT_%=;\\n}" :: "r"(sg_bar_a) : "memory");')
         B(f"  const int q_end = min(starts[bin + 1], item.y + {cfg.chunk});")
         B("  int qq = item.y + threadIdx.x;")
-        B("  float4 q4n = qq < q_end ? __ldg(&sorted[qq]) : make_float4(0.f, 0.f, 0.f, 0.f);")
+        B(f"  float4 q4n = qq < q_end ? {ldf}(&sorted[qq]) : make_float4(0.f, 0.f, 0.f, 0.f);")
         B(f"  for (; qq < q_end; qq += {cfg.block}) {{")
         B("  const float4 q4 = q4n;")
-        B(f"  if (qq + {cfg.block} < q_end) q4n = __ldg(&sorted[qq + {cfg.block}]);   // prefetch the next record")
+        B(f"  if (qq + {cfg.block} < q_end) q4n = {ldf}(&sorted[qq + {cfg.block}]);   // prefetch the next record")
         B("  const long long qi = (long long)__float_as_int(q4.w);")
         comps = ["x", "y", "z"]
         for d in range(s):
@@ -1487,10 +1494,10 @@ def generate(space, config: GenConfig | None = None, extents=None,
             body.append("    const long long qc = valid ? qi : n - 1;")
             for d in range(s):
                 if intsel:
-                    body.append(f"    const float xq{d} = xs[qc * {s} + {d}];")
+                    body.append(f"    const float xq{d} = {ldf}(&xs[qc * {s} + {d}]);")
                     body.append(f"    const double x{d} = (double)xq{d};")
                 else:
-                    body.append(f"    const double x{d} = (double)xs[qc * {s} + {d}];")
+                    body.append(f"    const double x{d} = (double){ldf}(&xs[qc * {s} + {d}]);")
             if intsel:
                 body.extend("    " + ln for ln in int_prelude())
             sctx["r"] = r
@@ -1560,14 +1567,14 @@ def generate(space, config: GenConfig | None = None, extents=None,
             body.append("      float4 a_ = sg_res4[ql];")
             for l in range(1, M):
                 body.append(f"      {{ const float4 b_ = sg_res4[{l * TQ} + ql]; a_.x += b_.x; a_.y += b_.y; a_.z += b_.z; a_.w += b_.w; }}")
-            body.append("      out[qi] = a_.x;")
+            body.append(f"      {stf}(&out[qi], a_.x);")
             for d in range(s):
-                body.append(f"      grad[qi * {s} + {d}] = a_.{'yzw'[d]};")
+                body.append(f"      {stf}(&grad[qi * {s} + {d}], a_.{'yzw'[d]});")
         else:
             expr = "sg_res[ql]"
             for l in range(1, M):
                 expr = f"({expr} + sg_res[{l * TQ} + ql])"
-            body.append(f"      out[qi] = 0.0f + {expr};")
+            body.append(f"      {stf}(&out[qi], 0.0f + {expr});")
         body.append("    }")
         body.append("    __syncthreads();")
         body.append("  }")   # tile loop
@@ -1594,10 +1601,10 @@ def generate(space, config: GenConfig | None = None, extents=None,
         em.line("}")
     if not sorted_:
         body += em.lines
-        body.append("  out[qi] = acc;")
+        body.append(f"  {stf}(&out[qi], acc);")
         if cfg.grad:
             for d in range(s):
-                body.append(f"  grad[qi * {s} + {d}] = gacc{d};")
+                body.append(f"  {stf}(&grad[qi * {s} + {d}], gacc{d});")
         body.append("  }")   # query loop (grid-stride in direct mode, chunk loop in binned mode)
         body.append("}")
     if lut:

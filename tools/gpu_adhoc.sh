@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-python -c "import __graft_entry__ as g; g.build(); g.smoke()" 2>&1 | tail -2
-timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -4
-echo "== variants c4v"; timeout 600 python tools/variants.py c4v --reps 10 2>&1 | grep -E "Grecon|FAIL|Error"
+python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -1
+for c in c4 c4v c3 c2 c1; do echo "== $c"; timeout 600 python tools/variants.py $c --reps 20 --only stream 2>&1 | grep -E "Grecon|FAIL|Error"; timeout 600 python tools/variants.py $c --reps 20 --only default 2>&1 | grep -E "Grecon|FAIL|Error"; done

@@ -38,6 +38,7 @@ VARIANTS = {
     "sorted_b512_t1536": dict(mode="sorted", block=512, tile=1536),
     "sorted_b512_t2048": dict(mode="sorted", block=512, tile=2048),
     "sglobal": dict(sigma_smem=0),
+    "nostream": dict(stream="default"),
 }
 
 
