@@ -419,17 +419,18 @@ __global__ void __launch_bounds__(1024) sg_bin_scan_small(int* __restrict__ mat,
 
 // K3': tile-local counting sort before the scatter: records of one bin leave the CTA as
 // contiguous runs (coalesced 16-B stores) instead of one scattered store per query.
-constexpr int SG_TILE = 4096;
+constexpr int SG_TILE = 4096;   // records per tile of the 1024-thread instantiation
 constexpr int SG_TILED_MAX_BINS = 2048;   // per-tile histogram cost grows with the bin count
 
-__global__ void __launch_bounds__(1024) sg_bin_scatter_tiled(
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) sg_bin_scatter_tiled(
     const float* __restrict__ xs, long long n, long long per, BinGeom g,
     const int* __restrict__ mat, float4* __restrict__ sorted) {
   extern __shared__ __align__(16) unsigned char shb[];
   const int nb = (int)g.nbins;
-  float4* tile = reinterpret_cast<float4*>(shb);                 // SG_TILE records
-  int* tbin = reinterpret_cast<int*>(tile + SG_TILE);              // SG_TILE bins
-  int* gpos = tbin + SG_TILE;                                      // nb: global cursor
+  float4* tile = reinterpret_cast<float4*>(shb);                 // (4 * THREADS) records
+  int* tbin = reinterpret_cast<int*>(tile + (4 * THREADS));              // (4 * THREADS) bins
+  int* gpos = tbin + (4 * THREADS);                                      // nb: global cursor
   int* lcnt = gpos + nb;                                           // nb: tile counts
   int* loff = lcnt + nb;                                           // nb: tile offsets
   __shared__ int scan_sh[32];
@@ -447,11 +448,11 @@ __global__ void __launch_bounds__(1024) sg_bin_scatter_tiled(
     pb = X4[1];
     pc = X4[2];
   }
-  for (long long t0 = lo; t0 < hi; t0 += SG_TILE) {
-    const int tn = (int)min((long long)SG_TILE, hi - t0);
+  for (long long t0 = lo; t0 < hi; t0 += (4 * THREADS)) {
+    const int tn = (int)min((long long)(4 * THREADS), hi - t0);
     const float4 ca = pa, cb = pb, cc = pc;
     {
-      const long long nx = t0 + SG_TILE + q0;
+      const long long nx = t0 + (4 * THREADS) + q0;
       if (vec && nx + 4 <= hi) {
         const float4* X4 = reinterpret_cast<const float4*>(xs + nx * 3);
         pa = __ldg(X4);
@@ -491,7 +492,7 @@ __global__ void __launch_bounds__(1024) sg_bin_scatter_tiled(
     __syncthreads();
     // B: tile offsets (exclusive scan over bins)
     {
-      const int per_t = (nb + 1023) / 1024;
+      const int per_t = (nb + THREADS - 1) / THREADS;
       const int b0 = threadIdx.x * per_t, b1 = min(nb, b0 + per_t);
       int mine = 0;
       for (int b = b0; b < b1; ++b) mine += lcnt[b];
@@ -902,7 +903,29 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
                 nb, SG_SMEM_BINS);
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, m->device);
-  const long long G = std::max<long long>(1, std::min<long long>((n + 32767) / 32768, 2LL * dev_sms));
+  // sort CTAs: `sort_ctas_per_sm` per SM (env SPLINEGPU_SORT_CTAS, default 2) of
+  // `scatter_threads` threads (env SPLINEGPU_SCATTER_THREADS: 1024 | 512 | 256)
+  static const int scatter_threads_env = [] {
+    const char* e = getenv("SPLINEGPU_SCATTER_THREADS");
+    const int v = e ? atoi(e) : 0;
+    return (v == 256 || v == 512 || v == 1024) ? v : 0;
+  }();
+  static const long long min_per = [] {   // queries per sort CTA at least (env SPLINEGPU_SORT_MINPER)
+    const char* e = getenv("SPLINEGPU_SORT_MINPER");
+    const long long v = e ? atoll(e) : 8192;
+    return v >= 1024 ? v : 8192;
+  }();
+  static const int sort_ctas_per_sm = [] {
+    const char* e = getenv("SPLINEGPU_SORT_CTAS");
+    const int v = e ? atoi(e) : 2;
+    return v >= 1 && v <= 16 ? v : 2;
+  }();
+  const long long G = std::max<long long>(
+      1, std::min<long long>((n + min_per - 1) / min_per, (long long)sort_ctas_per_sm * dev_sms));
+  // measured on B200: long per-CTA ranges (>= 32K queries) scatter best with 512-thread
+  // tiles, short ones with 1024-thread tiles (fewer barriers per query)
+  const int scatter_threads = scatter_threads_env ? scatter_threads_env
+                                                  : ((n + G - 1) / G >= 32768 ? 512 : 1024);
   const long long per = ((n + G - 1) / G + 3) & ~3LL;   // multiple of 4: float4 query groups
   const long long mlen = (long long)nb * G;
   const long long ntiles = (mlen + SG_SCAN_TILE - 1) / SG_SCAN_TILE;
@@ -938,9 +961,12 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
                          2 * SG_SMEM_BINS * sizeof(int));
     cudaFuncSetAttribute(sg_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          SG_SMEM_BINS * sizeof(int));
-    cudaFuncSetAttribute(sg_bin_scatter_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         SG_TILE * (sizeof(float4) + sizeof(int)) +
-                             3 * SG_TILED_MAX_BINS * sizeof(int));
+    cudaFuncSetAttribute(sg_bin_scatter_tiled<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         4096 * (sizeof(float4) + sizeof(int)) + 3 * SG_TILED_MAX_BINS * sizeof(int));
+    cudaFuncSetAttribute(sg_bin_scatter_tiled<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         2048 * (sizeof(float4) + sizeof(int)) + 3 * SG_TILED_MAX_BINS * sizeof(int));
+    cudaFuncSetAttribute(sg_bin_scatter_tiled<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         1024 * (sizeof(float4) + sizeof(int)) + 3 * SG_TILED_MAX_BINS * sizeof(int));
   });
   sg_bin_count<<<(unsigned)G, SG_SORT_THREADS, nb * sizeof(int), st>>>((const float*)xs, (long long)n,
                                                                       per, g, mat);
@@ -958,9 +984,16 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
   }
   CU(cudaGetLastError());
   if (nb <= (size_t)SG_TILED_MAX_BINS) {
-    const size_t shb = SG_TILE * (sizeof(float4) + sizeof(int)) + 3 * nb * sizeof(int);
-    sg_bin_scatter_tiled<<<(unsigned)G, 1024, shb, st>>>((const float*)xs, (long long)n, per, g,
-                                                        mat, sorted);
+    const size_t shb = 4 * scatter_threads * (sizeof(float4) + sizeof(int)) + 3 * nb * sizeof(int);
+    if (scatter_threads == 256)
+      sg_bin_scatter_tiled<256><<<(unsigned)G, 256, shb, st>>>((const float*)xs, (long long)n, per,
+                                                              g, mat, sorted);
+    else if (scatter_threads == 512)
+      sg_bin_scatter_tiled<512><<<(unsigned)G, 512, shb, st>>>((const float*)xs, (long long)n, per,
+                                                              g, mat, sorted);
+    else
+      sg_bin_scatter_tiled<1024><<<(unsigned)G, 1024, shb, st>>>((const float*)xs, (long long)n,
+                                                                per, g, mat, sorted);
   } else {
     sg_bin_scatter<<<(unsigned)G, SG_SORT_THREADS, nb * sizeof(int), st>>>(
         (const float*)xs, (long long)n, per, g, mat, sorted);
