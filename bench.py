@@ -59,6 +59,13 @@ CONFIGS = {
     "c4v": dict(space="fcc_voronoi2", extents=(161, 161, 161), queries=1 << 26, kind="uniform",
                 grad=True, scaling="weak", variant=dict(mode="direct", coeffs="table", block=128),
                 desc="FCC Voronoi spline (order 2), 4x161^3, 2^26 uniform, value + gradient"),
+    "c3r": dict(space="bcc_voronoi2", extents=(203, 203, 203), queries=1 << 26, kind="render",
+                rays=(512, 512, 256), grad=False, scaling="weak", variant=dict(block=128),
+                desc="fused volume render of c3: 512x512 rays x 256 samples through 2x203^3 BCC "
+                     "Voronoi (ray march + reconstruction + compositing in one kernel)"),
+    "c3rs": dict(space="bcc_voronoi2", extents=(203, 203, 203), queries=1 << 26, kind="render",
+                 rays=(512, 512, 256), grad=True, scaling="weak", variant=dict(block=128),
+                 desc="c3r with gradient (Lambert) shading at every sample"),
     "c5": dict(space="bcc_voronoi2", extents=(406, 406, 406), queries=1 << 30, kind="rays",
                rays=(1024, 1024, 1024), grad=False, scaling="strong",
                variant=dict(mode="direct", coeffs="imm", block=128),
@@ -100,9 +107,17 @@ def build_program(cfg_name, **over):
 def precompile_bench_kernels():
     from paper_2102_08518_b200.runtime import compile_source
     for name, c in CONFIGS.items():
-        if _space_available(c["space"]):
+        if not _space_available(c["space"]):
+            continue
+        if c["kind"] == "render":
+            from paper_2102_08518_b200 import generate, load_fixture
+            from paper_2102_08518_b200.render import render_config
+            space = load_fixture(c["space"])
+            prog = generate(space, render_config(space, c["grad"], **c.get("variant", {})),
+                            c["extents"])
+        else:
             _, prog = build_program(name)
-            compile_source(prog.source)
+        compile_source(prog.source)
 
 
 def falg_per_query(space_name):
@@ -449,6 +464,101 @@ def run_ours(args, rank, world, device):
     return line
 
 
+def run_render(args, rank, world, device):
+    """Fused renderer configs: one step = one image."""
+    import torch
+    from paper_2102_08518_b200 import load_fixture
+    from paper_2102_08518_b200.render import Renderer
+    c = CONFIGS[args.config]
+    space = load_fixture(c["space"])
+    rng = np.random.default_rng(0)
+    arrays = [rng.random(c["extents"]).astype(np.float32) for _ in range(space.ncosets)]
+    w, h, steps = c["rays"]
+    r = Renderer(space, arrays, w, h, steps, shade=c["grad"], device=device.index, **c.get("variant", {}))
+    stream = torch.cuda.current_stream(device)
+    for _ in range(args.warmup):
+        r.launch(stream)
+    torch.cuda.synchronize(device)
+    r.ev.module.status()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize(device)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(device.index) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            r.launch(stream)
+        e1.record(stream)
+        torch.cuda.synchronize(device)
+    ms = e0.elapsed_time(e1)
+    tt = torch.tensor([ms], dtype=torch.float64, device=device)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms = float(tt.item())
+    n = r.samples
+    value = n * world * args.steps / (ms / 1e3) / 1e9
+    step_ms = ms / args.steps
+    # end to end: rays from pinned host memory, render, image back to the host, every step
+    from paper_2102_08518_b200 import runtime
+    rays_h = torch.from_numpy(r.rays_np).pin_memory()
+    img_h = torch.empty((w * h, 4), dtype=torch.float32).pin_memory()
+    e2e_steps = max(3, min(args.steps, 20))
+    torch.cuda.synchronize(device)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        r.rays.copy_(rays_h, non_blocking=True)
+        r.launch(stream)
+        img_h.copy_(r.rgba, non_blocking=True)
+        torch.cuda.synchronize(device)
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=device)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = n * world * e2e_steps / float(te.item()) / 1e9
+    r.ev.module.status()
+    if rank != 0:
+        return None
+    pk = peaks()
+    falg = falg_per_query(c["space"])
+    roof = roofline(args.config, falg, n, step_ms, step_ms, pk)
+    line = {
+        "metric": "G reconstructions/sec per B200 (fraction of FP32 roofline in roofline)",
+        "value": round(value, 4), "unit": "Grecon/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": True,
+        "scaling": c["scaling"], "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": args.config + ": " + c["desc"], "space": c["space"],
+                   "extents": list(c["extents"]), "cosets": space.ncosets, "image": [w, h],
+                   "samples_per_ray": steps, "samples_per_gpu": n, "shading": c["grad"],
+                   "parallelism": f"full image per GPU x{world}",
+                   "l2": "no query/result streams: samples are generated and consumed in registers"},
+        "e2e": {"value": round(e2e_value, 4), "unit": "Grecon/s",
+                "h2d_bytes_per_step": int(r.rays_np.nbytes), "d2h_bytes_per_step": w * h * 16,
+                "steps": e2e_steps, "path": "ray table H2D (pinned), sg_render, rgba D2H"},
+        "gpu_launches": args.steps,
+        "roofline": roof,
+        "clocks": clk.summary(),
+        "kernel": {"regs": r.ev.module.regs()[0], "mode": "render", "block": r.prog.block},
+    }
+    if not args.no_cpu:
+        from oracle import refeval
+        from oracle import render as orender
+        from paper_2102_08518_b200.model import SPACES_DIR
+        osp = refeval.load_space_file(SPACES_DIR / f"{c['space']}.json")
+        npx = 64
+        t0 = time.perf_counter()
+        orender.render(osp, arrays, r.rays_np[:npx], steps, r.tf_np, shade=c["grad"])
+        dt = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": npx * steps / dt / 1e9, "unit": "Grecon/s", "cores": 1,
+                                "kind": "port",
+                                "sample": f"{npx} rays x {steps} samples through oracle/render.py "
+                                          f"(numpy f64 restatement of the reference evaluator + "
+                                          f"compositing), 1 process, {dt:.2f}s"}
+    return line
+
+
 def run_reference(args, rank, world):
     """--impl reference: the reference's CPU evaluator (oracle port) on all host cores,
     each step a bounded sample of the configuration's query stream."""
@@ -460,6 +570,8 @@ def run_reference(args, rank, world):
     space = load_fixture(c["space"])
     rng = np.random.default_rng(0)
     arrays = [rng.random(c["extents"]).astype(np.float32) for _ in range(space.ncosets)]
+    if c["kind"] == "render":
+        return run_reference_render(args, c, space, arrays)
     xs = make_queries(args.config, 0, 1 << 18, "cpu").numpy()
     total_budget = 150.0                       # seconds for the whole --steps/--warmup run
     per_step = total_budget / (args.steps + args.warmup)
@@ -488,6 +600,38 @@ def run_reference(args, rank, world):
         "cpu_baseline": {**vals[-1], "value": v},
         "e2e": {"value": v, "unit": "Grecon/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+
+
+def run_reference_render(args, c, space, arrays):
+    """--impl reference for the renderer configs: the oracle renderer (reference evaluator
+    restatement + compositing) on a bounded number of rays per step, one process."""
+    from oracle import refeval
+    from oracle import render as orender
+    from paper_2102_08518_b200.model import SPACES_DIR
+    from paper_2102_08518_b200.queries import ray_table
+    from paper_2102_08518_b200.render import DEFAULT_TF, tf_vector
+    w, h, steps = c["rays"]
+    rays = ray_table(c["extents"], w, h, steps)
+    tf = tf_vector(**DEFAULT_TF)
+    osp = refeval.load_space_file(SPACES_DIR / f"{c['space']}.json")
+    arr = [a.astype(np.float64) for a in arrays]
+    npx = 32
+    vals = []
+    for i in range(args.warmup + args.steps):
+        sl = rays[(i * npx) % len(rays):(i * npx) % len(rays) + npx]
+        t0 = time.perf_counter()
+        orender.render(osp, arr, sl, steps, tf, shade=c["grad"])
+        if i >= args.warmup:
+            vals.append(len(sl) * steps / (time.perf_counter() - t0) / 1e9)
+    v = statistics.median(vals)
+    return {"impl": "reference", "metric": "G reconstructions/sec per B200 (fraction of FP32 roofline in roofline)",
+            "value": v, "unit": "Grecon/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": None, "higher_is_better": True, "scaling": c["scaling"], "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config + ": " + c["desc"], "space": c["space"]},
+            "cpu_baseline": {"value": v, "unit": "Grecon/s", "cores": 1, "kind": "port",
+                             "sample": f"{npx} rays x {steps} samples per step, oracle/render.py"},
+            "e2e": {"value": v, "unit": "Grecon/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
 def _cpu_worker_init(cfg_name, arrays, xs, shard):
@@ -522,7 +666,10 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=device)
-    line = run_ours(args, rank, world, device)
+    if CONFIGS[args.config]["kind"] == "render":
+        line = run_render(args, rank, world, device)
+    else:
+        line = run_ours(args, rank, world, device)
     if line:
         print(json.dumps(line), flush=True)
     if world > 1:

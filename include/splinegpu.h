@@ -84,7 +84,7 @@ typedef struct sg_module_info {
   int32_t static_smem;         /* informational: static shared memory of the kernel */
 } sg_module_info;
 
-enum { SG_MODE_DIRECT = 0, SG_MODE_BINNED = 1 };
+enum { SG_MODE_DIRECT = 0, SG_MODE_BINNED = 1, SG_MODE_RENDER = 2 };
 enum { SG_FLOOR = 0, SG_ROUND = 1 };
 
 int sg_version(void);
@@ -138,6 +138,17 @@ int sg_eval(sg_module* m, const sg_volume* v, const void* xs, int64_t n, void* o
  * recommended for full PCIe / C2C bandwidth. */
 int sg_eval_host(sg_module* m, const sg_volume* v, const void* xs_host, int64_t n,
                  void* out_host, void* grad_host, int64_t chunk);
+
+/* Fused volume rendering (SG_MODE_RENDER modules): the caller of the evaluation path in
+ * the paper's application -- ray march, reconstruction (+ gradient shading)
+ * and front-to-back compositing in one kernel, so samples never round-trip through HBM.
+ * rays: npix x 8 floats (origin xyz, direction xyz, t0, dt), 16-B aligned, device memory;
+ * sample j of a ray sits at o + (t0 + (j + 1/2) dt) d (fp32, round-to-nearest, no FMA).
+ * tf: 12 floats (f_lo, 1/(f_hi - f_lo), opacity per unit length, rgb at f_lo, rgb at f_hi,
+ * light direction xyz -- used when the module was generated with gradients).
+ * rgba: npix x 4 floats (premultiplied colour, opacity). */
+int sg_render(sg_module* m, const sg_volume* v, const float* rays, int64_t npix, int32_t steps,
+              const float* tf, float* rgba, void* stream);
 
 /* Replicate a volume onto other devices (peer copy over NVLink when available). */
 int sg_volume_replicate(const sg_volume* v, int device, void* stream, sg_volume** out);

@@ -1068,9 +1068,37 @@ static int launch(sg_module* m, const sg_volume* v, const void* xs, int64_t n, v
   return SG_OK;
 }
 
+int sg_render(sg_module* m, const sg_volume* v, const float* rays, int64_t npix, int32_t steps,
+              const float* tf, float* rgba, void* stream) {
+  if (!m || !v) return fail(SG_EINVAL, "NULL module or volume");
+  if (m->info.mode != SG_MODE_RENDER) return fail(SG_EINVAL, "module was not generated in render mode");
+  if (npix < 0 || steps < 0) return fail(SG_EINVAL, "negative pixel or step count");
+  if (npix == 0) return SG_OK;
+  if (!rays || !tf || !rgba) return fail(SG_EINVAL, "NULL rays/tf/rgba");
+  if (((uintptr_t)rays & 15) || ((uintptr_t)rgba & 15))
+    return fail(SG_EINVAL, "rays and rgba must be 16-byte aligned");
+  int rc = check_pair(m, v);
+  if (rc) return rc;
+  CU(cudaSetDevice(m->device));
+  SgCosets cs{};
+  for (int c = 0; c < v->ncosets; ++c) cs.base[c] = v->origin[c];
+  long long nn = (long long)npix;
+  int st = steps;
+  unsigned* err = m->d_err;
+  void* args[] = {(void*)&rays, (void*)&nn, (void*)&rgba, (void*)&tf, (void*)&st, (void*)&err,
+                  (void*)&cs};
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device);
+  long long grid = (nn + m->info.block - 1) / m->info.block;
+  grid = std::min(grid, (long long)sms * std::max(1, 2048 / m->info.block) * 4);
+  return timed_launch(m, (const void*)m->kernel, dim3((unsigned)grid), dim3(m->info.block), args, 0,
+                      (cudaStream_t)stream);
+}
+
 int sg_eval(sg_module* m, const sg_volume* v, const void* xs, int64_t n, void* out, void* grad,
             int32_t* dbg, void* stream) {
   if (!m || !v) return fail(SG_EINVAL, "NULL module or volume");
+  if (m->info.mode == SG_MODE_RENDER) return fail(SG_EINVAL, "render-mode modules are launched with sg_render");
   if (n < 0) return fail(SG_EINVAL, "negative point count");
   if (n > 0 && (!xs || !out)) return fail(SG_EINVAL, "NULL xs/out");
   if (m->info.has_dbg && n > 0 && !dbg) return fail(SG_EINVAL, "kernel writes dbg; pass a buffer");
@@ -1088,6 +1116,7 @@ int sg_eval_host(sg_module* m, const sg_volume* v, const void* xs_host, int64_t 
   if (n == 0) return SG_OK;
   if (!xs_host || !out_host) return fail(SG_EINVAL, "NULL xs/out");
   if (m->info.has_dbg) return fail(SG_EINVAL, "debug kernels are device-path only");
+  if (m->info.mode == SG_MODE_RENDER) return fail(SG_EINVAL, "render-mode modules are launched with sg_render");
   if (m->info.has_grad && !grad_host) return fail(SG_EINVAL, "kernel writes grad; pass a buffer");
   int rc = check_pair(m, v);
   if (rc) return rc;

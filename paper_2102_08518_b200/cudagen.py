@@ -78,8 +78,8 @@ class GenConfig:
             raise ValueError(f"coeffs must be one of {COEFFS}")
         if self.block % 32 or not 32 <= self.block <= 1024:
             raise ValueError("block must be a multiple of 32 in [32, 1024]")
-        if self.mode not in ("direct", "binned", "sorted"):
-            raise ValueError("mode must be 'direct', 'binned' or 'sorted'")
+        if self.mode not in ("direct", "binned", "sorted", "render"):
+            raise ValueError("mode must be 'direct', 'binned', 'sorted' or 'render'")
         if self.stream not in ("cs", "default"):
             raise ValueError("stream must be 'cs' or 'default'")
         if self.select not in ("auto", "f64", "int"):
@@ -474,6 +474,9 @@ def generate(space, config: GenConfig | None = None, extents=None,
     h = t.halo
     binned = cfg.mode == "binned"
     sorted_ = cfg.mode == "sorted"
+    render = cfg.mode == "render"
+    if render and (cfg.float_width != F32 or s != 3 or not (M == 1 or cfg.unroll_cosets)):
+        raise ValueError("render mode supports f32 kernels of dimension 3 with unrolled cosets")
     if sorted_:
         if cfg.float_width != F32 or s > 3:
             raise ValueError("sorted mode supports f32 kernels of dimension <= 3")
@@ -705,14 +708,21 @@ def generate(space, config: GenConfig | None = None, extents=None,
             out.append(f"const int lo{d}_ = (int)X{d}_ & 0x3fffffff;")
         return out
 
-    min_blocks = cfg.min_blocks or (2 if sorted_ else 0)   # sorted: 2 CTAs / SM by design
+    # sorted: 2 CTAs / SM by design; render: an explicit bound (ptxas otherwise caps at 48 regs)
+    min_blocks = cfg.min_blocks or (2 if sorted_ else (max(1, 256 // cfg.block) if render else 0))
     lb = f"{cfg.block}, {min_blocks}" if min_blocks else f"{cfg.block}"
     body = []
     B = body.append
     if not binned:
         B(f'extern "C" __global__ void __launch_bounds__({lb}) {ENTRY}(')
-        B(f"    const {T}* __restrict__ xs, long long n, {T}* __restrict__ out, {T}* __restrict__ grad,")
-        B("    int* __restrict__ dbg, unsigned* __restrict__ err, SgCosets vol) {")
+        if render:
+            # fused volume renderer: one ray per thread, `steps` samples,
+            # reconstruction (+ gradient shading) and front-to-back compositing in registers
+            B("    const float4* __restrict__ rays, long long n, float4* __restrict__ rgba,")
+            B("    const float* __restrict__ tf, int steps, unsigned* __restrict__ err, SgCosets vol) {")
+        else:
+            B(f"    const {T}* __restrict__ xs, long long n, {T}* __restrict__ out, {T}* __restrict__ grad,")
+            B("    int* __restrict__ dbg, unsigned* __restrict__ err, SgCosets vol) {")
         for name, ctype, vals in smem:
             B(f"  __shared__ __align__(16) {ctype} {name}[{len(vals)}];")
         for name, ctype, vals in smem:
@@ -748,6 +758,30 @@ def generate(space, config: GenConfig | None = None, extents=None,
             B("  __syncthreads();")
         if sorted_:
             pass
+        elif render:
+            B(f"  const float tf_lo = tf[0], tf_inv = tf[1], tf_op = tf[2];")
+            B("  const float c0lo = tf[3], c1lo = tf[4], c2lo = tf[5];")
+            B("  const float c0d = tf[6] - tf[3], c1d = tf[7] - tf[4], c2d = tf[8] - tf[5];")
+            if cfg.grad:
+                B("  const float L0 = tf[9], L1 = tf[10], L2 = tf[11];")
+            B(f"  for (long long qi = (long long)blockIdx.x * {cfg.block} + threadIdx.x; qi < n;")
+            B(f"       qi += (long long)gridDim.x * {cfg.block}) {{")
+            B("  const float4 ra = __ldg(&rays[2 * qi]), rb = __ldg(&rays[2 * qi + 1]);")
+            B("  const float o0 = ra.x, o1 = ra.y, o2 = ra.z, r0 = ra.w, r1 = rb.x, r2 = rb.y;")
+            B("  const float t0 = rb.z, rdt = rb.w;")
+            B("  const float aop = tf_op * rdt;")
+            B("  float C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;")
+            B("  #pragma unroll 1")
+            B("  for (int j = 0; j < steps; ++j) {")
+            # sample positions in round-to-nearest fp32 ops (no contraction): the oracle
+            # forms the same float32 expression
+            B("  const float tj = __fadd_rn(t0, __fmul_rn(__fadd_rn((float)j, 0.5f), rdt));")
+            for d in range(s):
+                B(f"  const float xq{d} = __fadd_rn(o{d}, __fmul_rn(tj, r{d}));")
+                B(f"  const double x{d} = (double)xq{d};")
+            if intsel:
+                body.extend("  " + ln for ln in int_prelude())
+            ind = "  "
         else:
           # grid-stride loop: the shared tables are staged once per CTA, not once per 128 queries
           B(f"  for (long long qi = (long long)blockIdx.x * {cfg.block} + threadIdx.x; qi < n;")
@@ -1599,7 +1633,25 @@ def generate(space, config: GenConfig | None = None, extents=None,
         emit_coset(None, True)
         em.indent = "  "
         em.line("}")
-    if not sorted_:
+    if render:
+        body += em.lines
+        body.append("  const float dn = fminf(fmaxf((acc - tf_lo) * tf_inv, 0.f), 1.f);")
+        body.append("  const float al = fminf(dn * aop, 1.f);")
+        if cfg.grad:
+            body.append("  const float gl = sqrtf(gacc0 * gacc0 + gacc1 * gacc1 + gacc2 * gacc2);")
+            body.append("  const float sh = gl > 0.f ? 0.3f + 0.7f * fabsf(gacc0 * L0 + gacc1 * L1 + gacc2 * L2) / gl : 1.f;")
+        else:
+            body.append("  const float sh = 1.f;")
+        body.append("  const float w = (1.f - A) * al * sh;")
+        body.append("  C0 += w * (c0lo + dn * c0d);")
+        body.append("  C1 += w * (c1lo + dn * c1d);")
+        body.append("  C2 += w * (c2lo + dn * c2d);")
+        body.append("  A += (1.f - A) * al;")
+        body.append("  }")   # sample loop
+        body.append(f"  {stf}(&rgba[qi], make_float4(C0, C1, C2, A));")
+        body.append("  }")   # ray loop
+        body.append("}")
+    elif not sorted_:
         body += em.lines
         body.append(f"  {stf}(&out[qi], acc);")
         if cfg.grad:

@@ -109,6 +109,50 @@ def rays(lo: int, hi: int, extents, width: int, height: int, steps: int, seed: i
     return pts.to(torch.float32)
 
 
+def ray_table(extents, width: int, height: int, steps: int, seed: int = 2):
+    """Per-pixel rays of the orthographic camera used by `rays`, for the fused renderer:
+    (width*height, 8) float32 rows (origin xyz, direction xyz, t0, dt) in 8 x 4-pixel
+    warp-tile order (row i is pixel pixel_of(i)); sample j of a ray is at
+    o + (t0 + (j + 1/2) dt) d, evaluated in float32."""
+    E = np.array(extents, dtype=np.float64)
+    d, up, right = camera(seed)
+    center = E / 2
+    corners = np.array([[x, y, z] for x in (0, E[0]) for y in (0, E[1]) for z in (0, E[2])])
+    pr = (corners - center) @ right
+    pu = (corners - center) @ up
+    r0, r1 = pr.min(), pr.max()
+    u0, u1 = pu.min(), pu.max()
+    half = float(np.linalg.norm(E)) / 2
+    px, py = pixel_of(np.arange(width * height), width)
+    a = r0 + (px + 0.5) * ((r1 - r0) / width)
+    b = u0 + (py + 0.5) * ((u1 - u0) / height)
+    origin = center[None, :] + a[:, None] * right[None, :] + b[:, None] * up[None, :]
+    with np.errstate(divide="ignore"):
+        inv = 1.0 / d
+    t1 = (0.0 - origin) * inv[None, :]
+    t2 = (E[None, :] - origin) * inv[None, :]
+    tmin = np.minimum(t1, t2).max(axis=1)
+    tmax = np.maximum(t1, t2).min(axis=1)
+    miss = tmax <= tmin
+    tmin = np.where(miss, -half, tmin)
+    tmax = np.where(miss, half, tmax)
+    out = np.empty((width * height, 8), dtype=np.float32)
+    out[:, 0:3] = origin
+    out[:, 3:6] = d[None, :]
+    out[:, 6] = tmin
+    out[:, 7] = (tmax - tmin) / steps
+    return out
+
+
+def pixel_of(i, width: int):
+    """(px, py) of row i of a tile-ordered per-pixel table (8 x 4-pixel warp tiles)."""
+    i = np.asarray(i)
+    lane = i % 32
+    tile = i // 32
+    tiles_x = width // 8
+    return (tile % tiles_x) * 8 + lane % 8, (tile // tiles_x) * 4 + lane // 8
+
+
 def ray_count(width, height, steps):
     return width * height * steps
 

@@ -85,6 +85,8 @@ EXPORTS = {
     "sg_module_timing": ([ctypes.c_void_p, ctypes.c_int], ctypes.c_int),
     "sg_module_kernel_time": ([ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
                                ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
+    "sg_render": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "sg_volume_replicate": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
                              ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
 }
@@ -185,7 +187,7 @@ class Module:
         for c, row in enumerate(prog.padded_extents):
             for d, e in enumerate(row):
                 info.padded_extents[c][d] = e
-        info.mode = 1 if prog.mode == "binned" else 0
+        info.mode = {"binned": 1, "render": 2}.get(prog.mode, 0)
         info.rounding = prog.rounding
         info.stage_tma = int(prog.stage_tma)
         info.smem_bytes = prog.smem_bytes
@@ -301,6 +303,13 @@ def eval_device(module: Module, volume: Volume, xs, out, grad=None, dbg=None, st
                          ctypes.c_void_p(grad.data_ptr() if grad is not None else 0),
                          ctypes.c_void_p(dbg.data_ptr() if dbg is not None else 0),
                          _stream_ptr(stream)))
+
+
+def render_device(module: Module, volume: Volume, rays, steps: int, tf, rgba, stream=None):
+    """Fused ray-march + reconstruction + compositing (render-mode modules, sg_render)."""
+    _check(lib().sg_render(module.handle, volume.handle, ctypes.c_void_p(rays.data_ptr()),
+                           rays.shape[0], int(steps), ctypes.c_void_p(tf.data_ptr()),
+                           ctypes.c_void_p(rgba.data_ptr()), _stream_ptr(stream)))
 
 
 def eval_host(module: Module, volume: Volume, xs: np.ndarray, out: np.ndarray,
