@@ -191,7 +191,6 @@ __device__ __forceinline__ int sg_bin_of(const float* __restrict__ xs, long long
 
 constexpr int SG_SORT_THREADS = 1024;
 constexpr int SG_SMEM_BINS = 16384;     // bins that fit the privatized shared histograms
-constexpr int SG_SCAN_TILE = 8192;      // elements per CTA in the device-wide scan
 
 __device__ __forceinline__ int sg_bin_xyz(float x, float y, float z, const BinGeom& g) {
   const float c[3] = {x, y, z};
@@ -245,11 +244,11 @@ __device__ __forceinline__ void sg_for_queries(const float* __restrict__ xs, lon
   }
 }
 
-// K1: per-CTA histogram of a contiguous query range -> mat[bin * G + cta] (no atomics
-// on global memory; the (bin, cta) matrix is scanned bin-major next).
+// K1: per-CTA histogram of a contiguous query range -> mat[bin * G + cta] (smem atomics),
+// and the per-bin totals (one global atomic per non-empty (CTA, bin)).
 __global__ void __launch_bounds__(SG_SORT_THREADS) sg_bin_count(
     const float* __restrict__ xs, long long n, long long per, BinGeom g,
-    int* __restrict__ mat) {
+    int* __restrict__ mat, int* __restrict__ bin_tot) {
   extern __shared__ int hist[];
   const int G = gridDim.x;
   for (int b = threadIdx.x; b < g.nbins; b += blockDim.x) hist[b] = 0;
@@ -260,31 +259,15 @@ __global__ void __launch_bounds__(SG_SORT_THREADS) sg_bin_count(
     atomicAdd(&hist[sg_bin_xyz(x, y, z, g)], 1);
   });
   __syncthreads();
-  for (int b = threadIdx.x; b < g.nbins; b += blockDim.x) mat[(long long)b * G + blockIdx.x] = hist[b];
-}
-
-// device-wide exclusive scan of `len` ints (3 phases: tile sums, scan of sums, rescan)
-__global__ void __launch_bounds__(1024) sg_scan_tiles(const int* __restrict__ in, long long len,
-                                                      int* __restrict__ tile_sums) {
-  __shared__ int red[32];
-  const long long base = (long long)blockIdx.x * SG_SCAN_TILE;
-  int sum = 0;
-  for (int k = threadIdx.x; k < SG_SCAN_TILE; k += 1024) {
-    long long i = base + k;
-    if (i < len) sum += in[i];
-  }
-  for (int o = 16; o; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    int v = red[threadIdx.x];
-    for (int o = 16; o; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    if (threadIdx.x == 0) tile_sums[blockIdx.x] = v;
+  for (int b = threadIdx.x; b < g.nbins; b += blockDim.x) {
+    const int h = hist[b];
+    mat[(long long)b * G + blockIdx.x] = h;
+    if (h) atomicAdd(&bin_tot[b], h);
   }
 }
 
+// block-wide exclusive scan (any multiple-of-32 block size up to 1024)
 __device__ __forceinline__ int sg_block_excl_scan(int v, int* sh, int* total) {
-  // 1024-thread exclusive scan via warp shuffles
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int x = v;
   for (int o = 1; o < 32; o <<= 1) {
@@ -308,62 +291,40 @@ __device__ __forceinline__ int sg_block_excl_scan(int v, int* sh, int* total) {
   return excl;
 }
 
-__global__ void __launch_bounds__(1024) sg_scan_sums(int* __restrict__ tile_sums, long long ntiles) {
-  __shared__ int sh[32];
-  int carry = 0;
-  for (long long b = 0; b < ntiles; b += 1024) {
-    long long i = b + threadIdx.x;
-    int v = i < ntiles ? tile_sums[i] : 0;
-    int tot;
-    int e = sg_block_excl_scan(v, sh, &tot);
-    if (i < ntiles) tile_sums[i] = e + carry;
-    carry += tot;
-  }
-}
 
-__global__ void __launch_bounds__(1024) sg_scan_apply(int* __restrict__ data, long long len,
-                                                      const int* __restrict__ tile_offs) {
-  __shared__ int sh[32];
-  const long long base = (long long)blockIdx.x * SG_SCAN_TILE;
-  int carry = tile_offs[blockIdx.x];
-  constexpr int PER = SG_SCAN_TILE / 1024;   // contiguous elements per thread
-  int v[PER];
-  int local = 0;
-  for (int k = 0; k < PER; ++k) {
-    long long i = base + (long long)threadIdx.x * PER + k;
-    v[k] = i < len ? data[i] : 0;
-    local += v[k];
-  }
-  int excl = sg_block_excl_scan(local, sh, nullptr) + carry;
-  for (int k = 0; k < PER; ++k) {
-    long long i = base + (long long)threadIdx.x * PER + k;
-    if (i < len) data[i] = excl;
-    excl += v[k];
-  }
-}
 
-// starts[bin] = offset of (bin, cta 0); starts[nbins] = n
-__global__ void sg_bin_starts(const int* __restrict__ mat, long long nbins, int G, long long n,
-                              int* __restrict__ starts) {
-  long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (b < nbins) starts[b] = mat[b * G];
-  if (b == nbins) starts[b] = (int)n;
-}
 
-// work items for the evaluation grid: (bin, first query) per chunk of a bin; -1 = idle CTA
-__global__ void __launch_bounds__(1024) sg_make_items(const int* __restrict__ starts, int nbins,
-                                                      int chunk, int2* __restrict__ items,
-                                                      int max_items) {
+
+// One CTA: bin starts (exclusive scan of the bin totals), the scatter cursors, the
+// evaluation work items; re-zeroes the totals for the next call.  Each scatter CTA then
+// reserves its (bin) ranges with one atomicAdd on the cursor per bin, so no scan of the
+// (bin x CTA) count matrix is needed.
+__global__ void __launch_bounds__(1024) sg_bin_plan(int* __restrict__ bin_tot, int nbins, long long n,
+                                                    int chunk, int* __restrict__ starts,
+                                                    int* __restrict__ cursor,
+                                                    int2* __restrict__ items, int max_items) {
   __shared__ int sh[32];
   const int per = (nbins + 1023) / 1024;
   const int lo = threadIdx.x * per, hi = min(nbins, lo + per);
   int mine = 0;
-  for (int b = lo; b < hi; ++b) mine += (starts[b + 1] - starts[b] + chunk - 1) / chunk;
+  for (int b = lo; b < hi; ++b) mine += bin_tot[b];
+  int at = sg_block_excl_scan(mine, sh, nullptr);
+  int nchunks = 0;
+  for (int b = lo; b < hi; ++b) {
+    const int t = bin_tot[b];
+    starts[b] = at;
+    cursor[b] = at;
+    bin_tot[b] = 0;
+    nchunks += (t + chunk - 1) / chunk;
+    at += t;
+  }
+  if (threadIdx.x == 1023) starts[nbins] = (int)n;
   int total;
-  int at = sg_block_excl_scan(mine, sh, &total);
+  int it = sg_block_excl_scan(nchunks, sh, &total);
+  __syncthreads();
   for (int b = lo; b < hi; ++b) {
     const int s0 = starts[b], s1 = starts[b + 1];
-    for (int q = s0; q < s1; q += chunk) items[at++] = make_int2(b, q);
+    for (int q = s0; q < s1; q += chunk) items[it++] = make_int2(b, q);
   }
   for (int i = total + threadIdx.x; i < max_items; i += 1024) items[i] = make_int2(-1, 0);
 }
@@ -371,11 +332,14 @@ __global__ void __launch_bounds__(1024) sg_make_items(const int* __restrict__ st
 // K3: scatter (x, y, z, index) records to their sorted positions
 __global__ void __launch_bounds__(SG_SORT_THREADS) sg_bin_scatter(
     const float* __restrict__ xs, long long n, long long per, BinGeom g,
-    const int* __restrict__ mat, float4* __restrict__ sorted) {
+    const int* __restrict__ mat, int* __restrict__ cursor, float4* __restrict__ sorted) {
   extern __shared__ int sh[];
-  int* cnt = sh;   // running position per bin, seeded with this CTA's global offsets
+  int* cnt = sh;   // running position per bin: this CTA's reserved range in each bin
   const int G = gridDim.x;
-  for (int b = threadIdx.x; b < g.nbins; b += blockDim.x) cnt[b] = mat[(long long)b * G + blockIdx.x];
+  for (int b = threadIdx.x; b < g.nbins; b += blockDim.x) {
+    const int c = mat[(long long)b * G + blockIdx.x];
+    cnt[b] = c ? atomicAdd(&cursor[b], c) : 0;
+  }
   __syncthreads();
   const long long lo = (long long)blockIdx.x * per;
   const long long hi = min(n, lo + per);
@@ -385,37 +349,6 @@ __global__ void __launch_bounds__(SG_SORT_THREADS) sg_bin_scatter(
   });
 }
 
-// fused small scan (one CTA): exclusive scan of the (bin, CTA) matrix, bin starts and
-// the evaluation work items -- replaces 5 launches when the matrix is small
-__global__ void __launch_bounds__(1024) sg_bin_scan_small(int* __restrict__ mat, long long mlen,
-                                                          int nbins, int G, long long n, int chunk,
-                                                          int* __restrict__ starts,
-                                                          int2* __restrict__ items, int max_items) {
-  __shared__ int sh[32];
-  const long long per = (mlen + 1023) / 1024;
-  const long long lo = threadIdx.x * per, hi = min(mlen, lo + per);
-  int mine = 0;
-  for (long long i = lo; i < hi; ++i) mine += mat[i];
-  int run = sg_block_excl_scan(mine, sh, nullptr);
-  for (long long i = lo; i < hi; ++i) {
-    const int v = mat[i];
-    mat[i] = run;
-    run += v;
-  }
-  __syncthreads();
-  for (int b = threadIdx.x; b < nbins; b += 1024) starts[b] = mat[(long long)b * G];
-  if (threadIdx.x == 0) starts[nbins] = (int)n;
-  __syncthreads();
-  const int pb = (nbins + 1023) / 1024;
-  const int b0 = threadIdx.x * pb, b1 = min(nbins, b0 + pb);
-  int nchunks = 0;
-  for (int b = b0; b < b1; ++b) nchunks += (starts[b + 1] - starts[b] + chunk - 1) / chunk;
-  int total;
-  int at = sg_block_excl_scan(nchunks, sh, &total);
-  for (int b = b0; b < b1; ++b)
-    for (int q = starts[b]; q < starts[b + 1]; q += chunk) items[at++] = make_int2(b, q);
-  for (int i = total + threadIdx.x; i < max_items; i += 1024) items[i] = make_int2(-1, 0);
-}
 
 // K3': tile-local counting sort before the scatter: records of one bin leave the CTA as
 // contiguous runs (coalesced 16-B stores) instead of one scattered store per query.
@@ -425,7 +358,7 @@ constexpr int SG_TILED_MAX_BINS = 2048;   // per-tile histogram cost grows with 
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) sg_bin_scatter_tiled(
     const float* __restrict__ xs, long long n, long long per, BinGeom g,
-    const int* __restrict__ mat, float4* __restrict__ sorted) {
+    const int* __restrict__ mat, int* __restrict__ cursor, float4* __restrict__ sorted) {
   extern __shared__ __align__(16) unsigned char shb[];
   const int nb = (int)g.nbins;
   float4* tile = reinterpret_cast<float4*>(shb);                 // (4 * THREADS) records
@@ -435,7 +368,10 @@ __global__ void __launch_bounds__(THREADS) sg_bin_scatter_tiled(
   int* loff = lcnt + nb;                                           // nb: tile offsets
   __shared__ int scan_sh[32];
   const int G = gridDim.x;
-  for (int b = threadIdx.x; b < nb; b += blockDim.x) gpos[b] = mat[(long long)b * G + blockIdx.x];
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    const int c = mat[(long long)b * G + blockIdx.x];
+    gpos[b] = c ? atomicAdd(&cursor[b], c) : 0;
+  }
   const long long lo = (long long)blockIdx.x * per;
   const long long hi = min(n, lo + per);
   const bool vec = g.dim == 3 && ((((uintptr_t)xs) & 15) == 0);
@@ -928,23 +864,26 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
                                                   : ((n + G - 1) / G >= 32768 ? 512 : 1024);
   const long long per = ((n + G - 1) / G + 3) & ~3LL;   // multiple of 4: float4 query groups
   const long long mlen = (long long)nb * G;
-  const long long ntiles = (mlen + SG_SCAN_TILE - 1) / SG_SCAN_TILE;
   const int chunk = std::max(32, in.chunk);
   const long long max_items = (n + chunk - 1) / chunk + (long long)nb;
-  const size_t need = (size_t)n * sizeof(float4) + ((size_t)mlen + ntiles + nb + 1) * sizeof(int) +
-                      (size_t)max_items * sizeof(int2) + 1024;
+  // layout: bin totals (kept zero between calls) | cursors | starts | count matrix | items | records
+  const size_t head = ((3 * nb + 1) * sizeof(int) + 15) & ~(size_t)15;
+  const size_t need = head + (((size_t)mlen * sizeof(int) + 15) & ~(size_t)15) +
+                      (size_t)max_items * sizeof(int2) + (size_t)n * sizeof(float4) + 512;
   if (m->bin_scratch_bytes < need) {
     if (m->bin_scratch) cudaFree(m->bin_scratch);
     m->bin_scratch = nullptr;
     m->bin_scratch_bytes = 0;
     CU(cudaMalloc(&m->bin_scratch, need));
+    CU(cudaMemset(m->bin_scratch, 0, head));
     m->bin_scratch_bytes = need;
   }
-  float4* sorted = (float4*)m->bin_scratch;
-  int* mat = (int*)(sorted + n);
-  int* tile_sums = mat + mlen;
-  int* starts = tile_sums + ntiles;
-  int2* items = (int2*)(((uintptr_t)(starts + nb + 1) + 15) & ~(uintptr_t)15);
+  int* bin_tot = (int*)m->bin_scratch;
+  int* cursor = bin_tot + nb;
+  int* starts = cursor + nb;
+  int* mat = (int*)((char*)m->bin_scratch + head);
+  int2* items = (int2*)((char*)mat + (((size_t)mlen * sizeof(int) + 15) & ~(size_t)15));
+  float4* sorted = (float4*)(((uintptr_t)(items + max_items) + 255) & ~(uintptr_t)255);
   BinGeom g{};
   g.dim = in.dim;
   g.bin = in.bin;
@@ -969,34 +908,25 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
                          1024 * (sizeof(float4) + sizeof(int)) + 3 * SG_TILED_MAX_BINS * sizeof(int));
   });
   sg_bin_count<<<(unsigned)G, SG_SORT_THREADS, nb * sizeof(int), st>>>((const float*)xs, (long long)n,
-                                                                      per, g, mat);
+                                                                      per, g, mat, bin_tot);
   CU(cudaGetLastError());
-  if (mlen <= 16384) {   // a single CTA only wins for tiny matrices (latency-bound otherwise)
-    sg_bin_scan_small<<<1, 1024, 0, st>>>(mat, mlen, (int)nb, (int)G, (long long)n, chunk, starts,
-                                          items, (int)max_items);
-  } else {
-    sg_scan_tiles<<<(unsigned)ntiles, 1024, 0, st>>>(mat, mlen, tile_sums);
-    sg_scan_sums<<<1, 1024, 0, st>>>(tile_sums, ntiles);
-    sg_scan_apply<<<(unsigned)ntiles, 1024, 0, st>>>(mat, mlen, tile_sums);
-    sg_bin_starts<<<(unsigned)((nb + 256) / 256), 256, 0, st>>>(mat, (long long)nb, (int)G,
-                                                                (long long)n, starts);
-    sg_make_items<<<1, 1024, 0, st>>>(starts, (int)nb, chunk, items, (int)max_items);
-  }
+  sg_bin_plan<<<1, 1024, 0, st>>>(bin_tot, (int)nb, (long long)n, chunk, starts, cursor, items,
+                                  (int)max_items);
   CU(cudaGetLastError());
   if (nb <= (size_t)SG_TILED_MAX_BINS) {
     const size_t shb = 4 * scatter_threads * (sizeof(float4) + sizeof(int)) + 3 * nb * sizeof(int);
     if (scatter_threads == 256)
       sg_bin_scatter_tiled<256><<<(unsigned)G, 256, shb, st>>>((const float*)xs, (long long)n, per,
-                                                              g, mat, sorted);
+                                                              g, mat, cursor, sorted);
     else if (scatter_threads == 512)
       sg_bin_scatter_tiled<512><<<(unsigned)G, 512, shb, st>>>((const float*)xs, (long long)n, per,
-                                                              g, mat, sorted);
+                                                              g, mat, cursor, sorted);
     else
       sg_bin_scatter_tiled<1024><<<(unsigned)G, 1024, shb, st>>>((const float*)xs, (long long)n,
-                                                                per, g, mat, sorted);
+                                                                per, g, mat, cursor, sorted);
   } else {
     sg_bin_scatter<<<(unsigned)G, SG_SORT_THREADS, nb * sizeof(int), st>>>(
-        (const float*)xs, (long long)n, per, g, mat, sorted);
+        (const float*)xs, (long long)n, per, g, mat, cursor, sorted);
   }
   CU(cudaGetLastError());
   SgCosets cs{};

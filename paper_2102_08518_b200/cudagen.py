@@ -879,14 +879,33 @@ def generate(space, config: GenConfig | None = None, extents=None,
         # coset-0 shift, wrapped, relative to the (approximately assigned) bin:
         # loc = k + rel lands in [0, brick) for every coset and stencil site
         rnd0 = rm0.rounding if rm0.shape == PARALLELEPIPED else ROUND_NEAREST
+
+        def kb_f64(pre):
+            for d in range(s):
+                if rnd0 == ROUND_NEAREST:
+                    B(f"{pre}kb{d} = __double2ll_rz(__dadd_rn(x{d}, copysign(0.5, x{d})));")
+                else:
+                    B(f"{pre}kb{d} = __double2ll_rd(x{d});")
+                e_ = ext[0][d]
+                B(f"{pre}kbw{d} = (int)kb{d};")
+                B(f"{pre}if ((unsigned)kbw{d} >= {e_}u) {{ long long m_ = kb{d} % {e_}LL; kbw{d} = (int)(m_ < 0 ? m_ + {e_}LL : m_); }}")
         for d in range(s):
-            if rnd0 == ROUND_NEAREST:
-                B(f"  const long long kb{d} = __double2ll_rz(__dadd_rn(x{d}, copysign(0.5, x{d})));")
-            else:
-                B(f"  const long long kb{d} = __double2ll_rd(x{d});")
+            B(f"  long long kb{d}; int kbw{d};")
+        if intsel:
+            # fast range (2^-7 <= x < E): the coset-0 shift in fixed point, 0 <= kb <= E
+            B("  if (fast_) {")
+            for d in range(s):
+                e_ = ext[0][d]
+                C = (1 << (FIX - 1)) if rnd0 == ROUND_NEAREST else 0
+                B(f"    const int kq{d} = hi{d}_ + ((lo{d}_ + {C}) >> 30);")
+                B(f"    kb{d} = kq{d}; kbw{d} = kq{d} >= {e_} ? kq{d} - {e_} : kq{d};")
+            B("  } else {")
+            kb_f64("    ")
+            B("  }")
+        else:
+            kb_f64("  ")
+        for d in range(s):
             e_ = ext[0][d]
-            B(f"  int kbw{d} = (int)kb{d};")
-            B(f"  if ((unsigned)kbw{d} >= {e_}u) {{ long long m_ = kb{d} % {e_}LL; kbw{d} = (int)(m_ < 0 ? m_ + {e_}LL : m_); }}")
             B(f"  int u{d}_ = kbw{d} - lo{d};")
             B(f"  if (u{d}_ < -1) u{d}_ += {e_}; else if (u{d}_ > {bin_}) u{d}_ -= {e_};")
             B(f"  const long long rel{d} = (long long)(u{d}_ + {margin}) - kb{d};")

@@ -28,7 +28,9 @@ def main():
         if r[mi] == "gpu__time_duration.sum":
             v *= {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(r[ui], 1.0)
         per[int(r[ii])][r[mi]] = v
-        names[int(r[ii])] = r[ki].split("(")[0]
+        nm = r[ki].split("(")[0]
+        nm = nm[5:] if nm.startswith("void ") else nm
+        names[int(r[ii])] = nm
     # our kernels only (sg_*); the last `steps` evaluation launches and everything between
     ours = [k for k in sorted(per) if names[k].startswith("sg_")]
     evals = [k for k in ours if names[k] == "sg_eval_kernel"]

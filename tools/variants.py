@@ -39,6 +39,9 @@ VARIANTS = {
     "sorted_b512_t2048": dict(mode="sorted", block=512, tile=2048),
     "sglobal": dict(sigma_smem=0),
     "nostream": dict(stream="default"),
+    "chunk8k": dict(chunk=8192),
+    "chunk16k": dict(chunk=16384),
+    "chunk2k": dict(chunk=2048),
 }
 
 
