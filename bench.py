@@ -68,7 +68,7 @@ CONFIGS = {
                  desc="c3r with gradient (Lambert) shading at every sample"),
     "c5": dict(space="bcc_voronoi2", extents=(406, 406, 406), queries=1 << 30, kind="rays",
                rays=(1024, 1024, 1024), grad=False, scaling="strong",
-               variant=dict(mode="direct", coeffs="imm", block=128),
+               variant=dict(mode="sorted", coeffs="imm", block=512),
                desc="BCC Voronoi spline (order 2), 2x406^3, 2^30 ray-ordered sharded over the GPUs"),
 }
 DEFAULT_CONFIG = "c2"
@@ -661,11 +661,19 @@ def main():
         return 0
     import torch
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SPLINEGPU_DIST_BACKEND=gloo lets several ranks share one GPU (code-path checks of the
+    # multi-rank bench on a 1-GPU box); production runs use NCCL, one rank per GPU
+    backend = os.environ.get("SPLINEGPU_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local %= max(1, torch.cuda.device_count())
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=device)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
     if CONFIGS[args.config]["kind"] == "render":
         line = run_render(args, rank, world, device)
     else:

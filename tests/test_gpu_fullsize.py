@@ -79,3 +79,22 @@ def test_direct_and_binned_agree_full_size(cfg):
     _, p2 = bench.build_program(cfg, mode="direct")
     b = Evaluator(space, arrays, prog=p2)(xs)
     assert torch.equal(a, b) or float((a - b).abs().max()) <= 1e-6
+
+
+def test_multi_rank_bench_code_path():
+    """bench.py under torchrun with 2 ranks (gloo so both ranks can share the one GPU of
+    the test box): per-rank shards, volume broadcast, max-over-ranks timing, one line."""
+    import json
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, SPLINEGPU_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", "bench.py", "--gpus", "2",
+           "--config", "c1", "--steps", "3", "--warmup", "3", "--no-cpu"]
+    r = subprocess.run(cmd, cwd=str(bench.ROOT), env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["parallelism"].startswith("query shards x2")
