@@ -100,8 +100,37 @@ struct sg_module {
   size_t t_used = 0;
 };
 
+// Optional L2 residency control (env SPLINEGPU_L2_PERSIST=1): launches carry an access
+// policy window over the coefficient volume (persisting hits, streaming misses) so the
+// query/result streams cannot evict it.  Returns the persisting budget (0 = disabled).
+static size_t l2_persist_budget(int device) {
+  static std::mutex mu;
+  static int state[64] = {};      // 0 unknown, 1 off, 2 on
+  static size_t budget[64] = {};
+  static size_t max_window[64] = {};
+  std::lock_guard<std::mutex> lock(mu);
+  if (device < 0 || device >= 64) return 0;
+  if (state[device] == 0) {
+    state[device] = 1;
+    const char* e = getenv("SPLINEGPU_L2_PERSIST");
+    if (e && atoi(e) > 0) {
+      int mx = 0, win = 0;
+      cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, device);
+      cudaDeviceGetAttribute(&win, cudaDevAttrMaxAccessPolicyWindowSize, device);
+      if (mx > 0 && win > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)mx) == cudaSuccess) {
+        budget[device] = (size_t)mx;
+        max_window[device] = (size_t)win;
+        state[device] = 2;
+      }
+      cudaGetLastError();
+    }
+  }
+  return state[device] == 2 ? std::min(budget[device], max_window[device]) : 0;
+}
+
 static int timed_launch(sg_module* m, const void* func, dim3 grid, dim3 block, void** args,
-                        size_t smem, cudaStream_t st) {
+                        size_t smem, cudaStream_t st, const void* win_base = nullptr,
+                        size_t win_bytes = 0) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (m->timing) {
     std::lock_guard<std::mutex> lock(m->t_mu);
@@ -116,7 +145,27 @@ static int timed_launch(sg_module* m, const void* func, dim3 grid, dim3 block, v
     ++m->t_used;
     CU(cudaEventRecord(e0, st));
   }
-  CU(cudaLaunchKernel(func, grid, block, args, smem, st));
+  const size_t budget = win_base ? l2_persist_budget(m->device) : 0;
+  if (budget) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    const size_t nb = std::min(win_bytes, budget);
+    at[0].val.accessPolicyWindow.base_ptr = const_cast<void*>(win_base);
+    at[0].val.accessPolicyWindow.num_bytes = nb;
+    at[0].val.accessPolicyWindow.hitRatio = std::min(1.0f, (float)budget / (float)std::max<size_t>(nb, 1));
+    at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CU(cudaLaunchKernelExC(&cfg, func, args));
+  } else {
+    CU(cudaLaunchKernel(func, grid, block, args, smem, st));
+  }
   if (e1) CU(cudaEventRecord(e1, st));
   return SG_OK;
 }
@@ -994,7 +1043,7 @@ static int launch(sg_module* m, const sg_volume* v, const void* xs, int64_t n, v
   }
   grid = std::min(grid, cap);
   return timed_launch(m, (const void*)m->kernel, dim3((unsigned)grid), dim3(m->info.block), args,
-                      (size_t)std::max(0, m->info.smem_bytes), st);
+                      (size_t)std::max(0, m->info.smem_bytes), st, v->alloc, v->bytes);
   return SG_OK;
 }
 
@@ -1022,7 +1071,7 @@ int sg_render(sg_module* m, const sg_volume* v, const float* rays, int64_t npix,
   long long grid = (nn + m->info.block - 1) / m->info.block;
   grid = std::min(grid, (long long)sms * std::max(1, 2048 / m->info.block) * 4);
   return timed_launch(m, (const void*)m->kernel, dim3((unsigned)grid), dim3(m->info.block), args, 0,
-                      (cudaStream_t)stream);
+                      (cudaStream_t)stream, v->alloc, v->bytes);
 }
 
 int sg_eval(sg_module* m, const sg_volume* v, const void* xs, int64_t n, void* out, void* grad,

@@ -1,0 +1,124 @@
+"""Known-answer tests ported from the reference suite (SURVEY 8c list), run on the CUDA
+path through the C ABI (GPU) or on generated sources (CPU):
+
+  rho round / floor cases          reference tests/test_codegen.py:83-104
+  ZP quadrants + exact classification                      :135-157
+  refetch is bitwise equal                                 :247-258
+  branchy == predicated (K = 2)                            :238-244
+  fetch count == n * M                                     :395-402
+  shift invariance (integer steps, coset permutation)      tests/test_oracle.py:108-129
+"""
+
+from fractions import Fraction as F
+
+import numpy as np
+import pytest
+
+from tests.gpu_util import load_golden
+
+
+def _dbg_eval(name, xs, **kw):
+    import torch
+    from paper_2102_08518_b200 import Evaluator, GenConfig, ScheduleParams
+    space, _, _, arrays = load_golden(name)
+    ev = Evaluator(space, arrays, GenConfig(ScheduleParams(1, space.stencil_size), dbg=True, **kw))
+    out, _, dbg = ev(torch.tensor(xs, dtype=torch.float32).cuda())
+    return out.cpu().numpy(), dbg.cpu().numpy()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["direct", "binned", "sorted"])
+def test_rho_round_mode(mode):
+    _, dbg = _dbg_eval("zp", [[1.3, 2.7], [-0.2, 0.6]], mode=mode)
+    assert dbg[0, 0, :2].tolist() == [1, 3]
+    assert dbg[1, 0, :2].tolist() == [0, 1]
+
+
+@pytest.mark.gpu
+def test_rho_floor_mode():
+    _, dbg = _dbg_eval("linear1d", [[1.3], [-1.3]])
+    assert dbg[0, 0, 0] == 1 and dbg[1, 0, 0] == -2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["direct", "sorted"])
+def test_membership_zp_quadrants(mode):
+    _, dbg = _dbg_eval("zp", [[0.4, 0.1], [0.1, 0.4], [-0.4, -0.1], [0.1, -0.4]], mode=mode)
+    assert dbg[:, 0, 2].tolist() == [0, 1, 2, 3]
+
+
+@pytest.mark.gpu
+def test_membership_matches_exact_classification():
+    space, _, _, _ = load_golden("zp")
+    rng = np.random.default_rng(8)
+    pts = rng.uniform(-0.5, 0.5, size=(1000, 2)).astype(np.float32)
+    _, dbg = _dbg_eval("zp", pts)
+    for (x0, x1), sub in zip(pts, dbg[:, 0, 2]):
+        ex0, ex1 = F(float(x0)), F(float(x1))
+        q = (1 if ex0 - ex1 >= 0 else 0) | (2 if ex0 + ex1 >= 0 else 0)
+        assert space.indexer.sigma[q] == int(sub)
+
+
+def _values(name, xs, **kw):
+    import torch
+    from paper_2102_08518_b200 import Evaluator, GenConfig, ScheduleParams
+    space, _, _, arrays = load_golden(name)
+    md = kw.pop("md", (1, space.stencil_size))
+    mode = kw.pop("branch", "predicated")
+    refetch = kw.pop("refetch", False)
+    data = kw.pop("arrays", arrays)
+    cfg = GenConfig(ScheduleParams(md[0], md[1], mode, refetch), **kw)
+    ev = Evaluator(space, data, cfg)
+    return ev(torch.as_tensor(np.asarray(xs, np.float32)).cuda()).cpu().numpy()
+
+
+@pytest.mark.gpu
+def test_refetch_is_bitwise_equal():
+    _, _, z, _ = load_golden("zp")
+    xs = z["uniform_xs"]
+    a = _values("zp", xs, md=(2, 4), form="sites")
+    b = _values("zp", xs, md=(2, 4), form="sites", refetch=True)
+    assert np.array_equal(a, b)
+
+
+@pytest.mark.gpu
+def test_branchy_equals_predicated_k2():
+    _, _, z, _ = load_golden("zp_k2")
+    xs = z["uniform_xs"]
+    a = _values("zp_k2", xs, md=(2, 4))
+    b = _values("zp_k2", xs, md=(2, 4), branch="branchy")
+    assert np.abs(a - b).max() <= 1e-6
+
+
+@pytest.mark.parametrize("name", ["zp", "trilinear", "halfgrid1d"])
+def test_fetch_count_equals_stencil_times_cosets(name):
+    from paper_2102_08518_b200 import GenConfig, ScheduleParams, generate
+    space, _, _, arrays = load_golden(name)
+    prog = generate(space, GenConfig(ScheduleParams(1, space.stencil_size)), arrays[0].shape)
+    assert prog.source.count("__ldg(V + (") == space.stencil_size * space.ncosets
+
+
+@pytest.mark.gpu
+def test_shift_invariance_integer_steps():
+    space, _, _, arrays = load_golden("zp")
+    rng = np.random.default_rng(12)
+    E = arrays[0].shape
+    pts = (rng.random((200, 2)) * np.array(E) * 0.5 + 1.0).astype(np.float32)
+    base = _values("zp", pts)
+    for z in [(1, 0), (0, 1), (2, 3), (-1, 2)]:
+        shifted = [np.roll(arrays[0], z, axis=(0, 1))]
+        got = _values("zp", pts + np.array(z, np.float32), arrays=shifted)
+        assert np.abs(got - base).max() <= 1e-5
+
+
+@pytest.mark.gpu
+def test_shift_invariance_permutes_cosets():
+    # generator 1/2: shifting the queries by half a cell swaps the cosets
+    # (c'_1 = c_0, c'_0 = roll(c_1, 1))
+    space, _, _, arrays = load_golden("halfgrid1d")
+    rng = np.random.default_rng(13)
+    pts = (rng.random((200, 1)) * (arrays[0].shape[0] - 2) + 1.0).astype(np.float32)
+    base = _values("halfgrid1d", pts)
+    shifted = [np.roll(arrays[1], 1), arrays[0]]
+    got = _values("halfgrid1d", pts + np.float32(0.5), arrays=shifted)
+    assert np.abs(got - base).max() <= 1e-5
