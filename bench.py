@@ -60,11 +60,11 @@ CONFIGS = {
                 grad=True, scaling="weak", variant=dict(mode="direct", coeffs="table", block=128),
                 desc="FCC Voronoi spline (order 2), 4x161^3, 2^26 uniform, value + gradient"),
     "c3r": dict(space="bcc_voronoi2", extents=(203, 203, 203), queries=1 << 26, kind="render",
-                rays=(512, 512, 256), grad=False, scaling="weak", variant=dict(block=128),
+                rays=(512, 512, 256), grad=False, scaling="weak", variant=dict(),
                 desc="fused volume render of c3: 512x512 rays x 256 samples through 2x203^3 BCC "
-                     "Voronoi (ray march + reconstruction + compositing in one kernel)"),
+                     "Voronoi (ray march + psi-sorted reconstruction + compositing in one kernel)"),
     "c3rs": dict(space="bcc_voronoi2", extents=(203, 203, 203), queries=1 << 26, kind="render",
-                 rays=(512, 512, 256), grad=True, scaling="weak", variant=dict(block=128),
+                 rays=(512, 512, 256), grad=True, scaling="weak", variant=dict(),
                  desc="c3r with gradient (Lambert) shading at every sample"),
     "c5": dict(space="bcc_voronoi2", extents=(406, 406, 406), queries=1 << 30, kind="rays",
                rays=(1024, 1024, 1024), grad=False, scaling="strong",

@@ -633,7 +633,7 @@ int sg_module_load(const void* image, size_t image_len, const char* entry, int d
       }
     }
   }
-  if (m->info.mode == SG_MODE_DIRECT && m->info.smem_bytes > 0) {
+  if ((m->info.mode == SG_MODE_DIRECT || m->info.mode == SG_MODE_RENDER) && m->info.smem_bytes > 0) {
     // sorted direct kernels keep their per-tile pair records in dynamic shared memory
     e = cudaFuncSetAttribute((const void*)m->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              m->info.smem_bytes);
@@ -1070,8 +1070,18 @@ int sg_render(sg_module* m, const sg_volume* v, const float* rays, int64_t npix,
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device);
   long long grid = (nn + m->info.block - 1) / m->info.block;
   grid = std::min(grid, (long long)sms * std::max(1, 2048 / m->info.block) * 4);
-  return timed_launch(m, (const void*)m->kernel, dim3((unsigned)grid), dim3(m->info.block), args, 0,
-                      (cudaStream_t)stream, v->alloc, v->bytes);
+  if (m->info.smem_bytes > 0) {
+    // psi-sorted renderer: persistent CTAs over blocks of 128 rays
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)m->kernel, m->info.block,
+                                                      (size_t)m->info.smem_bytes) != cudaSuccess ||
+        occ < 1)
+      occ = 1;
+    grid = std::min((nn + 127) / 128, (long long)sms * occ);
+  }
+  return timed_launch(m, (const void*)m->kernel, dim3((unsigned)grid), dim3(m->info.block), args,
+                      (size_t)std::max(0, m->info.smem_bytes), (cudaStream_t)stream, v->alloc,
+                      v->bytes);
 }
 
 int sg_eval(sg_module* m, const sg_volume* v, const void* xs, int64_t n, void* out, void* grad,

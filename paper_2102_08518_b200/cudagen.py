@@ -84,7 +84,7 @@ class GenConfig:
             raise ValueError("stream must be 'cs' or 'default'")
         if self.select not in ("auto", "f64", "int"):
             raise ValueError("select must be 'auto', 'f64' or 'int'")
-        if self.mode == "sorted" and (self.tile % self.block or self.tile > 8192 or self.tile < 0):
+        if self.mode in ("sorted", "render") and (self.tile % self.block or self.tile > 8192 or self.tile < 0):
             raise ValueError("sorted mode: tile must be a multiple of block and <= 8192")
         if self.stage not in ("tma", "ldg", "l1"):
             raise ValueError("stage must be 'tma', 'ldg' or 'l1' (no staging: sorted queries, L1 gathers)")
@@ -473,8 +473,13 @@ def generate(space, config: GenConfig | None = None, extents=None,
         raise ValueError(f"extents must give {s} values for each of {M} cosets")
     h = t.halo
     binned = cfg.mode == "binned"
-    sorted_ = cfg.mode == "sorted"
     render = cfg.mode == "render"
+    # sorted evaluation: mode "sorted", or the renderer with tile > 0 (samples of a block of
+    # RB rays x (tile / RB) steps are sorted by psi like queries of a sorted tile)
+    sorted_ = cfg.mode == "sorted" or (render and cfg.tile > 0)
+    RB = 128   # sorted render: rays per CTA block (four 8 x 4-pixel warp tiles)
+    if render and cfg.tile > 0 and (cfg.tile % RB or cfg.block % 32):
+        raise ValueError("sorted render: tile must be a multiple of 128 rays")
     if render and (cfg.float_width != F32 or s != 3 or not (M == 1 or cfg.unroll_cosets)):
         raise ValueError("render mode supports f32 kernels of dimension 3 with unrolled cosets")
     if sorted_:
@@ -750,10 +755,25 @@ def generate(space, config: GenConfig | None = None, extents=None,
             for l in range(M):
                 B(f"  const int coff{l} = (int)((const float*)vol.base[{l}] - (const float*)vol.base[0]);")
             B("  __syncthreads();")
-            # persistent tiles: the shared tables are staged once per CTA
-            B(f"  for (long long q0 = (long long)blockIdx.x * {TQ}; q0 < n; q0 += (long long)gridDim.x * {TQ}) {{")
             sorted_smem = MP * pair_bytes
             ind = "  "
+            if render:
+                B(f"  const float tf_lo = tf[0], tf_inv = tf[1], tf_op = tf[2];")
+                B("  const float c0lo = tf[3], c1lo = tf[4], c2lo = tf[5];")
+                B("  const float c0d = tf[6] - tf[3], c1d = tf[7] - tf[4], c2d = tf[8] - tf[5];")
+                if cfg.grad:
+                    B("  const float L0 = tf[9], L1 = tf[10], L2 = tf[11];")
+                # persistent ray blocks; each block marches its RB rays in chunks of SJ steps
+                B(f"  for (long long rb0 = (long long)blockIdx.x * {RB}; rb0 < n; rb0 += (long long)gridDim.x * {RB}) {{")
+                B(f"  const long long myray = rb0 + threadIdx.x;")
+                B(f"  float my_dt = 0.f;")
+                B(f"  if (threadIdx.x < {RB} && myray < n) my_dt = __ldg(&rays[2 * myray + 1]).w;")
+                B("  const float my_aop = tf_op * my_dt;")
+                B("  float C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;")
+                B(f"  for (int j0 = 0; j0 < steps; j0 += {TQ // RB}) {{")
+            else:
+                # persistent tiles: the shared tables are staged once per CTA
+                B(f"  for (long long q0 = (long long)blockIdx.x * {TQ}; q0 < n; q0 += (long long)gridDim.x * {TQ}) {{")
         elif smem:
             B("  __syncthreads();")
         if sorted_:
@@ -1542,10 +1562,23 @@ def generate(space, config: GenConfig | None = None, extents=None,
         for r in range(PQ):
             body.append(f"    {{  // query {r} of this thread in the tile")
             body.append(f"    const int ql = {r * Bk} + (int)threadIdx.x;")
-            body.append("    const long long qi = q0 + ql;")
-            body.append("    const bool valid = qi < n;")
-            body.append("    const long long qc = valid ? qi : n - 1;")
-            for d in range(s):
+            if render:
+                # sample (ray rb0 + ql % RB, step j0 + ql / RB): positions as in the unsorted
+                # renderer (round-to-nearest fp32 ops)
+                body.append(f"    const long long ray_ = rb0 + (ql % {RB});")
+                body.append(f"    const int j_ = j0 + ql / {RB};")
+                body.append("    const bool valid = ray_ < n && j_ < steps;")
+                body.append("    const long long rc_ = ray_ < n ? ray_ : n - 1;")
+                body.append("    const float4 ra = __ldg(&rays[2 * rc_]), rb = __ldg(&rays[2 * rc_ + 1]);")
+                body.append("    const float tj = __fadd_rn(rb.z, __fmul_rn(__fadd_rn((float)j_, 0.5f), rb.w));")
+                for d, (oc, dc) in enumerate((("ra.x", "ra.w"), ("ra.y", "rb.x"), ("ra.z", "rb.y"))):
+                    body.append(f"    const float xq{d} = __fadd_rn({oc}, __fmul_rn(tj, {dc}));")
+                    body.append(f"    const double x{d} = (double)xq{d};")
+            else:
+                body.append("    const long long qi = q0 + ql;")
+                body.append("    const bool valid = qi < n;")
+                body.append("    const long long qc = valid ? qi : n - 1;")
+            for d in range(s if not render else 0):
                 if intsel:
                     body.append(f"    const float xq{d} = {ldf}(&xs[qc * {s} + {d}]);")
                     body.append(f"    const double x{d} = (double)xq{d};")
@@ -1612,6 +1645,42 @@ def generate(space, config: GenConfig | None = None, extents=None,
             body.append("      sg_res[pi_] = acc;")
         body.append("    }")
         body.append("    __syncthreads();")
+        if render:
+            # phase 3 (render): each of the RB first threads composites its ray's SJ samples
+            # front to back (coset contributions summed in coset order)
+            body.append(f"    if (threadIdx.x < {RB}) {{")
+            body.append(f"      for (int jj = 0; jj < {TQ // RB} && j0 + jj < steps; ++jj) {{")
+            body.append(f"        const int ql = jj * {RB} + (int)threadIdx.x;")
+            if cfg.grad:
+                body.append("        float4 a_ = sg_res4[ql];")
+                for l in range(1, M):
+                    body.append(f"        {{ const float4 b_ = sg_res4[{l * TQ} + ql]; a_.x += b_.x; a_.y += b_.y; a_.z += b_.z; a_.w += b_.w; }}")
+                body.append("        const float acc = a_.x, gacc0 = a_.y, gacc1 = a_.z, gacc2 = a_.w;")
+            else:
+                expr = "sg_res[ql]"
+                for l in range(1, M):
+                    expr = f"({expr} + sg_res[{l * TQ} + ql])"
+                body.append(f"        const float acc = 0.0f + {expr};")
+            body.append("        const float dn = fminf(fmaxf((acc - tf_lo) * tf_inv, 0.f), 1.f);")
+            body.append("        const float al = fminf(dn * my_aop, 1.f);")
+            if cfg.grad:
+                body.append("        const float gl = sqrtf(gacc0 * gacc0 + gacc1 * gacc1 + gacc2 * gacc2);")
+                body.append("        const float sh = gl > 0.f ? 0.3f + 0.7f * fabsf(gacc0 * L0 + gacc1 * L1 + gacc2 * L2) / gl : 1.f;")
+            else:
+                body.append("        const float sh = 1.f;")
+            body.append("        const float w = (1.f - A) * al * sh;")
+            body.append("        C0 += w * (c0lo + dn * c0d);")
+            body.append("        C1 += w * (c1lo + dn * c1d);")
+            body.append("        C2 += w * (c2lo + dn * c2d);")
+            body.append("        A += (1.f - A) * al;")
+            body.append("      }")
+            body.append("    }")
+            body.append("    __syncthreads();")
+            body.append("  }")   # step chunks
+            body.append(f"  if (threadIdx.x < {RB} && myray < n) {stf}(&rgba[myray], make_float4(C0, C1, C2, A));")
+            body.append("  }")   # ray blocks
+            body.append("}")
+    if sorted_ and not render:
         # phase 3: coset contributions summed in coset order, coalesced stores
         body.append(f"    for (int ql = threadIdx.x; ql < {TQ}; ql += {Bk}) {{")
         body.append("      const long long qi = q0 + ql;")
@@ -1632,6 +1701,8 @@ def generate(space, config: GenConfig | None = None, extents=None,
         body.append("    __syncthreads();")
         body.append("  }")   # tile loop
         body.append("}")
+    elif sorted_:
+        pass
     elif M == 1:
         em.line("{")
         em.indent = "    "
@@ -1652,7 +1723,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
         emit_coset(None, True)
         em.indent = "  "
         em.line("}")
-    if render:
+    if render and not sorted_:
         body += em.lines
         body.append("  const float dn = fminf(fmaxf((acc - tf_lo) * tf_inv, 0.f), 1.f);")
         body.append("  const float al = fminf(dn * aop, 1.f);")

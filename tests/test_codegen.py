@@ -56,10 +56,12 @@ def test_sorted_mode_rejects_unsupported_configs():
 
 @pytest.mark.parametrize("name", [n for n in golden_names() if load_golden(n)[0].dim == 3])
 @pytest.mark.parametrize("shade", [False, True])
-def test_render_kernel_generates_and_compiles(name, shade):
+@pytest.mark.parametrize("variant", ["march", "sorted"])
+def test_render_kernel_generates_and_compiles(name, shade, variant):
     from paper_2102_08518_b200.render import render_config
     space, _, _, arrays = load_golden(name)
-    prog = generate(space, render_config(space, shade), arrays[0].shape)
+    kw = dict(block=128, tile=512) if variant == "sorted" else {}
+    prog = generate(space, render_config(space, shade, **kw), arrays[0].shape)
     assert prog.mode == "render" and prog.has_grad == shade
     _, key = compile_source(prog.source)
     spills = [int(v) for v in re.findall(r"(\d+) bytes spill stores", ptxas_info(key))]

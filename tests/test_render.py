@@ -39,11 +39,14 @@ def test_oracle_composite_limits():
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", ["bcc_voronoi2", "bcc_box5", "fcc_box6", "tricubic", "fcc_voronoi2"])
 @pytest.mark.parametrize("shade", [False, True])
-def test_render_matches_oracle(name, shade):
+@pytest.mark.parametrize("variant", ["march", "sorted"])
+def test_render_matches_oracle(name, shade, variant):
     import torch
     from paper_2102_08518_b200.render import Renderer
     space, ospace, z, arrays = load_golden(name)
-    r = Renderer(space, arrays, 16, 8, 24, shade=shade)
+    kw = dict(block=128, tile=512) if variant == "sorted" else {}
+    # 16 x 8 pixels = one 128-ray block; 24 steps = 6 chunks of 4 steps in the sorted kernel
+    r = Renderer(space, arrays, 16, 8, 24, shade=shade, **kw)
     img = r().cpu().numpy().reshape(-1, 4)
     want = orender.render(ospace, arrays, r.rays_np, 24, r.tf_np, shade=shade)
     px, py = pixel_of(np.arange(16 * 8), 16)

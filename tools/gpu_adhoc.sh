@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -1
-timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q -k "binned or c1 or c2" 2>&1 | tail -3
-for c in c2 c1; do echo "== $c"; timeout 600 python tools/variants.py $c --reps 30 --only chunk 2>&1 | grep -E "Grecon|FAIL|Error"; timeout 600 python tools/variants.py $c --reps 30 --only default 2>&1 | grep -E "Grecon|FAIL|Error"; done
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_c2_r01c.csv python bench.py --config c2 --steps 3 --warmup 3 --no-cpu > /dev/null 2>&1
+timeout 900 python -m pytest tests/test_render.py -x -q 2>&1 | tail -3
+for c in c3r c3rs; do echo "== $c"; timeout 600 python tools/variants.py $c --reps 10 2>&1 | grep -E "Gsamples|FAIL|Error"; done

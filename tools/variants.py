@@ -20,6 +20,16 @@ import bench  # noqa: E402
 from paper_2102_08518_b200 import Evaluator, load_fixture  # noqa: E402
 from paper_2102_08518_b200 import runtime  # noqa: E402
 
+RENDER_VARIANTS = {
+    "march": dict(),
+    "sorted_b256_t1536": dict(block=256, tile=1536),
+    "sorted_b256_t1024": dict(block=256, tile=1024),
+    "sorted_b512_t1536": dict(block=512, tile=1536),
+    "sorted_b512_t2048": dict(block=512, tile=2048),
+    "sorted_b128_t1024": dict(block=128, tile=1024),
+    "sorted_b384_t1536": dict(block=384, tile=1536),
+}
+
 VARIANTS = {
     "default": dict(),
     "table": dict(coeffs="table"),
@@ -52,6 +62,8 @@ def main():
     ap.add_argument("--reps", type=int, default=50)
     a = ap.parse_args()
     c = bench.CONFIGS[a.config]
+    if c["kind"] == "render":
+        return render_variants(a, c)
     dev = torch.device("cuda", 0)
     space, arrays, xs = bench.make_inputs(a.config, 0, dev)
     n = xs.shape[0]
@@ -91,6 +103,39 @@ def main():
         diff = float((out - ref).abs().max())
         print(f"{name:28s} {ms:8.4f} ms (eval {kms / max(kn, 1):7.4f})  {n / ms / 1e6:8.3f} Grecon/s"
               f"  regs {ev.module.regs()[0]:3d}  maxdiff-vs-first {diff:.2e}", flush=True)
+
+
+def render_variants(a, c):
+    from paper_2102_08518_b200.render import Renderer
+    space = load_fixture(c["space"])
+    rng = np.random.default_rng(0)
+    arrays = [rng.random(c["extents"]).astype(np.float32) for _ in range(space.ncosets)]
+    w, h, steps = c["rays"]
+    ref = None
+    for name, over in RENDER_VARIANTS.items():
+        if a.only and a.only not in name:
+            continue
+        try:
+            r = Renderer(space, arrays, w, h, steps, shade=c["grad"], **over)
+        except Exception as e:  # noqa: BLE001
+            print(f"{name:28s} FAILED {e}")
+            continue
+        for _ in range(3):
+            r.launch()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(a.reps):
+            r.launch()
+        s1.record()
+        torch.cuda.synchronize()
+        ms = s0.elapsed_time(s1) / a.reps
+        r.ev.module.status()
+        img = r().clone()
+        if ref is None:
+            ref = img
+        print(f"{name:28s} {ms:8.4f} ms  {r.samples / ms / 1e6:8.3f} Gsamples/s  regs {r.ev.module.regs()[0]:3d}"
+              f"  maxdiff-vs-first {float((img - ref).abs().max()):.2e}", flush=True)
 
 
 if __name__ == "__main__":
