@@ -60,7 +60,7 @@ def test_sorted_mode_rejects_unsupported_configs():
 def test_render_kernel_generates_and_compiles(name, shade, variant):
     from paper_2102_08518_b200.render import render_config
     space, _, _, arrays = load_golden(name)
-    kw = dict(block=128, tile=512) if variant == "sorted" else {}
+    kw = dict(block=128, tile=512) if variant == "sorted" else dict(block=128, tile=0)
     prog = generate(space, render_config(space, shade, **kw), arrays[0].shape)
     assert prog.mode == "render" and prog.has_grad == shade
     _, key = compile_source(prog.source)

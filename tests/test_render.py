@@ -44,7 +44,7 @@ def test_render_matches_oracle(name, shade, variant):
     import torch
     from paper_2102_08518_b200.render import Renderer
     space, ospace, z, arrays = load_golden(name)
-    kw = dict(block=128, tile=512) if variant == "sorted" else {}
+    kw = dict(block=128, tile=512) if variant == "sorted" else dict(block=128, tile=0)
     # 16 x 8 pixels = one 128-ray block; 24 steps = 6 chunks of 4 steps in the sorted kernel
     r = Renderer(space, arrays, 16, 8, 24, shade=shade, **kw)
     img = r().cpu().numpy().reshape(-1, 4)
