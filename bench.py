@@ -447,15 +447,15 @@ def run_ours(args, rank, world, device):
                 "d2h_bytes_per_step": n * 4 * (1 + (space.dim if grad is not None else 0)),
                 "steps": e2e_steps, "path": "sg_eval_host (C ABI, pinned host buffers, "
                 "H2D / kernel / D2H pipelined over 2^22-query chunks)"},
-        "gpu_launches": args.steps * (8 if prog.mode == "binned" else 1),
+        "gpu_launches": args.steps * (4 if prog.mode == "binned" else 1),
         "roofline": roof,
         "clocks": clk.summary(),
         "kernel": {"regs": ev.module.regs()[0], "fetch_mode": prog.meta["fetch_mode"],
                    "form": prog.config.form, "coeffs": prog.config.coeffs, "mode": prog.mode,
                    "bin": prog.bin, "brick": list(prog.brick), "block": prog.block,
                    "eval_kernel_ms": round(eval_kernel_ms, 4), "wall_s": round(t_wall, 3)},
-        "gpu_launches_note": "per step: binning (count, 3-phase scan, starts, items, scatter) "
-                             "+ the evaluation kernel" if prog.mode == "binned" else "1 kernel per step",
+        "gpu_launches_note": "per step: query sort (sg_bin_count, sg_bin_plan, sg_bin_scatter_tiled) "
+                             "+ sg_eval_kernel" if prog.mode == "binned" else "1 kernel per step",
     }
     if not args.no_cpu:
         xs_np = xs[: 1 << 20].cpu().numpy()
