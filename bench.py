@@ -405,12 +405,16 @@ def run_ours(args, rank, world, device):
     e2e_steps = max(3, min(args.steps, 20))
     lib = runtime.lib()
 
+    # 2^22-query chunks: H2D, kernel and D2H overlap on 3 streams for the large configs;
+    # smaller chunks cost more in per-call fixed work (measured: c1 2^18 chunks 1.3 vs 1.8)
+    host_chunk = 1 << 22
+
     def host_step():
         runtime._check(lib.sg_eval_host(ev.module.handle, ev.volume.handle,
                                         runtime.ctypes.c_void_p(xs_host.data_ptr()), n,
                                         runtime.ctypes.c_void_p(out_host.data_ptr()),
                                         runtime.ctypes.c_void_p(grad_host.data_ptr() if grad_host is not None else 0),
-                                        1 << 22))
+                                        host_chunk))
     host_step()
     if world > 1:
         dist.barrier()
@@ -446,7 +450,7 @@ def run_ours(args, rank, world, device):
                 "h2d_bytes_per_step": n * space.dim * 4,
                 "d2h_bytes_per_step": n * 4 * (1 + (space.dim if grad is not None else 0)),
                 "steps": e2e_steps, "path": "sg_eval_host (C ABI, pinned host buffers, "
-                "H2D / kernel / D2H pipelined over 2^22-query chunks)"},
+                f"H2D / kernel / D2H pipelined over {host_chunk}-query chunks on 3 streams)"},
         "gpu_launches": args.steps * (4 if prog.mode == "binned" else 1),
         "roofline": roof,
         "clocks": clk.summary(),
