@@ -225,18 +225,6 @@ struct BinGeom {
   long long nbins;
 };
 
-__device__ __forceinline__ int sg_bin_of(const float* __restrict__ xs, long long i,
-                                         const BinGeom& g) {
-  int lin = 0;
-  for (int d = 0; d < g.dim; ++d) {
-    float x = xs[i * g.dim + d];
-    float xw = x - g.ext[d] * floorf(x * g.inv_ext[d]);   // wrap into [0, E) (approximately)
-    int b = (int)floorf(xw * g.inv_bin);
-    b = min(max(b, 0), g.nb[d] - 1);
-    lin = lin * g.nb[d] + b;
-  }
-  return lin;
-}
 
 constexpr int SG_SORT_THREADS = 1024;
 constexpr int SG_SMEM_BINS = 16384;     // bins that fit the privatized shared histograms
@@ -256,17 +244,6 @@ __device__ __forceinline__ int sg_bin_xyz(float x, float y, float z, const BinGe
   return lin;
 }
 
-// warp-aggregated shared-memory atomic: lanes with the same bin share one atomicAdd
-__device__ __forceinline__ int sg_agg_add(int* counters, int b) {
-  const unsigned act = __activemask();
-  const unsigned peers = __match_any_sync(act, b);
-  const int lane = threadIdx.x & 31;
-  const int leader = __ffs(peers) - 1;
-  int base = 0;
-  if (lane == leader) base = atomicAdd(&counters[b], __popc(peers));
-  base = __shfl_sync(peers, base, leader);
-  return base + __popc(peers & ((1u << lane) - 1));
-}
 
 // Queries of a CTA range are read as float4 triples (4 queries of 3 floats) when the
 // range is 16-B aligned; `visit(i, x, y, z)` is called for every query.

@@ -41,6 +41,8 @@ def test_invalid_arguments_fail_without_gpu():
     assert rc == runtime.SG_EINVAL
     rc = lib.sg_eval(None, None, None, 0, None, None, None, None)
     assert rc == runtime.SG_EINVAL
+    rc = lib.sg_render(None, None, None, 0, 0, None, None, None)
+    assert rc == runtime.SG_EINVAL
 
 
 def test_nvrtc_compiles_for_sm100a_without_gpu():

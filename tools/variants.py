@@ -49,6 +49,12 @@ VARIANTS = {
     "sorted_b512_t2048": dict(mode="sorted", block=512, tile=2048),
     "sglobal": dict(sigma_smem=0),
     "nostream": dict(stream="default"),
+    "occ_128x8": dict(block=128, min_blocks=8),
+    "occ_128x10": dict(block=128, min_blocks=10),
+    "occ_256x4": dict(block=256, min_blocks=4),
+    "occ_256x5": dict(block=256, min_blocks=5),
+    "sorted_b1024_t3072": dict(mode="sorted", block=1024, tile=3072),
+    "sorted_b512_t1536x": dict(mode="sorted", block=512, tile=1536),
     "chunk8k": dict(chunk=8192),
     "chunk16k": dict(chunk=16384),
     "chunk2k": dict(chunk=2048),
