@@ -68,6 +68,7 @@ class GenConfig:
     stream: str = "cs"           # query/result cache policy: "cs" (evict-first) | "default"
     select: str = "auto"         # selection arithmetic: "f64" | "int" (2^-30 fixed point) | "auto"
     sigma_smem: int = 4096       # sigma tables up to this many entries are staged in smem
+    pack: int = 1                # 2: two queries per thread, polynomial FP in packed f32x2 (FFMA2)
 
     def __post_init__(self):
         if self.float_width not in (F64, F32):
@@ -80,6 +81,8 @@ class GenConfig:
             raise ValueError("block must be a multiple of 32 in [32, 1024]")
         if self.mode not in ("direct", "binned", "sorted", "render"):
             raise ValueError("mode must be 'direct', 'binned', 'sorted' or 'render'")
+        if self.pack not in (1, 2):
+            raise ValueError("pack must be 1 or 2")
         if self.stream not in ("cs", "default"):
             raise ValueError("stream must be 'cs' or 'default'")
         if self.select not in ("auto", "f64", "int"):
@@ -322,6 +325,74 @@ class Emitter:
     def line(self, text):
         self.lines.append(self.indent + text)
 
+    def tree2(self, node, u, c):
+        """Packed (float2) emission of a Horner tree for two queries at once: FFMA2 / FADD2 /
+        FMUL2 with broadcast immediates; a product feeding exactly one sum is fused."""
+        uses = {}
+        stack = [node]
+        seen = set()
+        while stack:
+            nd = stack.pop()
+            if id(nd) in seen:
+                continue
+            seen.add(id(nd))
+            if isinstance(nd, (Add, Mul)):
+                for ch in (nd.left, nd.right):
+                    uses[id(ch)] = uses.get(id(ch), 0) + 1
+                    stack.append(ch)
+        out = {}
+        fused = {}
+
+        def lit(q):
+            v = flit(q, F32)
+            return f"make_float2({v}, {v})"
+        stack = [(node, False)]
+        while stack:
+            nd, done = stack.pop()
+            key = id(nd)
+            if key in out:
+                continue
+            if isinstance(nd, Const):
+                out[key] = lit(nd.value)
+            elif isinstance(nd, Var):
+                out[key] = u[nd.index]
+            elif isinstance(nd, Sym):
+                out[key] = c[nd.index]
+            elif not done:
+                stack.append((nd, True))
+                if isinstance(nd, Add):
+                    # one product used only here is emitted inside the FMA: visit its operands
+                    fz = fused.get(key)
+                    if fz is None:
+                        fz = next((ch for ch in (nd.left, nd.right) if isinstance(ch, Mul)
+                                   and uses.get(id(ch), 0) == 1 and id(ch) not in out), False)
+                        fused[key] = fz
+                    for ch in (nd.right, nd.left):
+                        if fz is not False and ch is fz:
+                            stack.append((ch.right, False))
+                            stack.append((ch.left, False))
+                        else:
+                            stack.append((ch, False))
+                else:
+                    stack.append((nd.right, False))
+                    stack.append((nd.left, False))
+            else:
+                t = self.tmp("p")
+                if isinstance(nd, Add):
+                    l, r = nd.left, nd.right
+                    fz = fused.get(key, False)
+                    if fz is not False:
+                        m, other = (l, r) if fz is l else (r, l)
+                        expr = (f"__ffma2_rn({out[id(m.left)]}, {out[id(m.right)]}, "
+                                f"{out[id(other)]})")
+                    else:
+                        expr = f"__fadd2_rn({out[id(l)]}, {out[id(r)]})"
+                else:
+                    expr = f"__fmul2_rn({out[id(nd.left)]}, {out[id(nd.right)]})"
+                self.line(f"const float2 {t} = {expr};")
+                out[key] = t
+        return out[id(node)]
+
     def tree(self, node, u, c, consts=None):
         """Post-order emission of a Horner tree; returns the operand string."""
         out = {}
@@ -478,6 +549,14 @@ def generate(space, config: GenConfig | None = None, extents=None,
     # RB rays x (tile / RB) steps are sorted by psi like queries of a sorted tile)
     sorted_ = cfg.mode == "sorted" or (render and cfg.tile > 0)
     RB = 128   # sorted render: rays per CTA block (four 8 x 4-pixel warp tiles)
+    pack2 = cfg.pack == 2
+    if pack2:
+        if cfg.float_width != F32 or cfg.mode not in ("direct", "binned"):
+            raise ValueError("pack=2 supports f32 kernels in direct or binned mode")
+        if not (M == 1 or cfg.unroll_cosets) or cfg.coeffs != "imm":
+            raise ValueError("pack=2 needs unrolled cosets and immediate coefficients")
+        if len(space.ref_polys) > 1 and cfg.params.branch_mode != PREDICATED:
+            raise ValueError("pack=2 evaluates every reference polynomial (predicated dispatch)")
     if render and cfg.tile > 0 and (cfg.tile % RB or cfg.block % 32):
         raise ValueError("sorted render: tile must be a multiple of 128 rays")
     if render and (cfg.float_width != F32 or s != 3 or not (M == 1 or cfg.unroll_cosets)):
@@ -700,6 +779,66 @@ def generate(space, config: GenConfig | None = None, extents=None,
         A(f"__device__ const int sg_sigma_g[{len(t.sigma)}] = {{{', '.join(str(v) for v in t.sigma)}}};")
 
     # ---- kernel -------------------------------------------------------------
+    def direct_preamble(pre="  "):
+        """Per query (direct mode): the query point from xs[qi] + the fixed-point split."""
+        out = []
+        for d in range(s):
+            if intsel:
+                out.append(f"{pre}const float xq{d} = {ldf}(&xs[qi * {s} + {d}]);")
+                out.append(f"{pre}const double x{d} = (double)xq{d};")
+            else:
+                out.append(f"{pre}const double x{d} = (double){ldf}(&xs[qi * {s} + {d}]);")
+        if intsel:
+            out.extend(pre + ln for ln in int_prelude())
+        return out
+
+    def binned_preamble(pre="  "):
+        """Per query (binned mode, record q4 in scope): original index, point, fixed-point
+        split, and the coset-0 shift relative to the (approximately assigned) bin:
+        loc = k + rel lands in [0, brick) for every coset and stencil site."""
+        out = []
+        Q = out.append
+        Q(f"{pre}const long long qi = (long long)__float_as_int(q4.w);")
+        comps = ["x", "y", "z"]
+        for d in range(s):
+            if intsel:
+                Q(f"{pre}const float xq{d} = q4.{comps[d]};")
+            Q(f"{pre}const double x{d} = (double)q4.{comps[d]};")
+        if intsel:
+            out.extend(pre + ln for ln in int_prelude())
+        rnd0 = rm0.rounding if rm0.shape == PARALLELEPIPED else ROUND_NEAREST
+
+        def kb_f64(p2):
+            for d in range(s):
+                if rnd0 == ROUND_NEAREST:
+                    Q(f"{p2}kb{d} = __double2ll_rz(__dadd_rn(x{d}, copysign(0.5, x{d})));")
+                else:
+                    Q(f"{p2}kb{d} = __double2ll_rd(x{d});")
+                e_ = ext[0][d]
+                Q(f"{p2}kbw{d} = (int)kb{d};")
+                Q(f"{p2}if ((unsigned)kbw{d} >= {e_}u) {{ long long m_ = kb{d} % {e_}LL; kbw{d} = (int)(m_ < 0 ? m_ + {e_}LL : m_); }}")
+        for d in range(s):
+            Q(f"{pre}long long kb{d}; int kbw{d};")
+        if intsel:
+            # fast range (2^-7 <= x < E): the coset-0 shift in fixed point, 0 <= kb <= E
+            Q(f"{pre}if (fast_) {{")
+            for d in range(s):
+                e_ = ext[0][d]
+                C = (1 << (FIX - 1)) if rnd0 == ROUND_NEAREST else 0
+                Q(f"{pre}  const int kq{d} = hi{d}_ + ((lo{d}_ + {C}) >> 30);")
+                Q(f"{pre}  kb{d} = kq{d}; kbw{d} = kq{d} >= {e_} ? kq{d} - {e_} : kq{d};")
+            Q(f"{pre}}} else {{")
+            kb_f64(pre + "  ")
+            Q(f"{pre}}}")
+        else:
+            kb_f64(pre)
+        for d in range(s):
+            e_ = ext[0][d]
+            Q(f"{pre}int u{d}_ = kbw{d} - lo{d};")
+            Q(f"{pre}if (u{d}_ < -1) u{d}_ += {e_}; else if (u{d}_ > {bin_}) u{d}_ -= {e_};")
+            Q(f"{pre}const long long rel{d} = (long long)(u{d}_ + {margin}) - kb{d};")
+        return out
+
     def int_prelude():
         """Per query: fixed-point split x = hi + lo * 2^-30 (lo in [0, 2^30)), exact for the
         fast-path range 2^-7 <= x < E (so 0 <= k <= E: one conditional subtract wraps it);
@@ -714,7 +853,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
         return out
 
     # sorted: 2 CTAs / SM by design; render: an explicit bound (ptxas otherwise caps at 48 regs)
-    min_blocks = cfg.min_blocks or (2 if sorted_ else (max(1, 256 // cfg.block) if render else 0))
+    min_blocks = cfg.min_blocks or (2 if sorted_ else (max(1, 256 // cfg.block) if (render or pack2) else 0))
     lb = f"{cfg.block}, {min_blocks}" if min_blocks else f"{cfg.block}"
     body = []
     B = body.append
@@ -804,16 +943,13 @@ def generate(space, config: GenConfig | None = None, extents=None,
             ind = "  "
         else:
           # grid-stride loop: the shared tables are staged once per CTA, not once per 128 queries
-          B(f"  for (long long qi = (long long)blockIdx.x * {cfg.block} + threadIdx.x; qi < n;")
-          B(f"       qi += (long long)gridDim.x * {cfg.block}) {{")
-          for d in range(s):
-              if intsel:
-                  B(f"  const float xq{d} = {ldf}(&xs[qi * {s} + {d}]);")
-                  B(f"  const double x{d} = (double)xq{d};")
-              else:
-                  B(f"  const double x{d} = (double){ldf}(&xs[qi * {s} + {d}]);")
-          if intsel:
-              body.extend("  " + ln for ln in int_prelude())
+          if pack2:
+              B(f"  for (long long q0_ = (long long)blockIdx.x * {2 * cfg.block}; q0_ < n;")
+              B(f"       q0_ += (long long)gridDim.x * {2 * cfg.block}) {{")
+          else:
+              B(f"  for (long long qi = (long long)blockIdx.x * {cfg.block} + threadIdx.x; qi < n;")
+              B(f"       qi += (long long)gridDim.x * {cfg.block}) {{")
+              body.extend(direct_preamble())
           ind = "  "
     else:
         B(f'extern "C" __global__ void __launch_bounds__({lb}) {ENTRY}(')
@@ -883,54 +1019,17 @@ def generate(space, config: GenConfig | None = None, extents=None,
         if cfg.stage == "tma" and smem_fetch:
             B('  asm volatile("{\\n .reg .pred p;\\n SG_WAIT_%=:\\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\\n @!p bra SG_WAIT_%=;\\n}" :: "r"(sg_bar_a) : "memory");')
         B(f"  const int q_end = min(starts[bin + 1], item.y + {cfg.chunk});")
-        B("  int qq = item.y + threadIdx.x;")
-        B(f"  float4 q4n = qq < q_end ? {ldf}(&sorted[qq]) : make_float4(0.f, 0.f, 0.f, 0.f);")
-        B(f"  for (; qq < q_end; qq += {cfg.block}) {{")
-        B("  const float4 q4 = q4n;")
-        B(f"  if (qq + {cfg.block} < q_end) q4n = {ldf}(&sorted[qq + {cfg.block}]);   // prefetch the next record")
-        B("  const long long qi = (long long)__float_as_int(q4.w);")
-        comps = ["x", "y", "z"]
-        for d in range(s):
-            if intsel:
-                B(f"  const float xq{d} = q4.{comps[d]};")
-            B(f"  const double x{d} = (double)q4.{comps[d]};")
-        if intsel:
-            body.extend("  " + ln for ln in int_prelude())
-        # coset-0 shift, wrapped, relative to the (approximately assigned) bin:
-        # loc = k + rel lands in [0, brick) for every coset and stencil site
-        rnd0 = rm0.rounding if rm0.shape == PARALLELEPIPED else ROUND_NEAREST
-
-        def kb_f64(pre):
-            for d in range(s):
-                if rnd0 == ROUND_NEAREST:
-                    B(f"{pre}kb{d} = __double2ll_rz(__dadd_rn(x{d}, copysign(0.5, x{d})));")
-                else:
-                    B(f"{pre}kb{d} = __double2ll_rd(x{d});")
-                e_ = ext[0][d]
-                B(f"{pre}kbw{d} = (int)kb{d};")
-                B(f"{pre}if ((unsigned)kbw{d} >= {e_}u) {{ long long m_ = kb{d} % {e_}LL; kbw{d} = (int)(m_ < 0 ? m_ + {e_}LL : m_); }}")
-        for d in range(s):
-            B(f"  long long kb{d}; int kbw{d};")
-        if intsel:
-            # fast range (2^-7 <= x < E): the coset-0 shift in fixed point, 0 <= kb <= E
-            B("  if (fast_) {")
-            for d in range(s):
-                e_ = ext[0][d]
-                C = (1 << (FIX - 1)) if rnd0 == ROUND_NEAREST else 0
-                B(f"    const int kq{d} = hi{d}_ + ((lo{d}_ + {C}) >> 30);")
-                B(f"    kb{d} = kq{d}; kbw{d} = kq{d} >= {e_} ? kq{d} - {e_} : kq{d};")
-            B("  } else {")
-            kb_f64("    ")
-            B("  }")
+        if pack2:
+            B(f"  for (int qq = item.y + threadIdx.x; qq < q_end; qq += {2 * cfg.block}) {{")
         else:
-            kb_f64("  ")
-        for d in range(s):
-            e_ = ext[0][d]
-            B(f"  int u{d}_ = kbw{d} - lo{d};")
-            B(f"  if (u{d}_ < -1) u{d}_ += {e_}; else if (u{d}_ > {bin_}) u{d}_ -= {e_};")
-            B(f"  const long long rel{d} = (long long)(u{d}_ + {margin}) - kb{d};")
+            B("  int qq = item.y + threadIdx.x;")
+            B(f"  float4 q4n = qq < q_end ? {ldf}(&sorted[qq]) : make_float4(0.f, 0.f, 0.f, 0.f);")
+            B(f"  for (; qq < q_end; qq += {cfg.block}) {{")
+            B("  const float4 q4 = q4n;")
+            B(f"  if (qq + {cfg.block} < q_end) q4n = {ldf}(&sorted[qq + {cfg.block}]);   // prefetch the next record")
+            body.extend(binned_preamble())
         ind = "  "
-    if not sorted_:
+    if not sorted_ and not pack2:
         B(f"{ind}{T} acc = ({T})0;")
         if cfg.grad:
             for d in range(s):
@@ -1297,6 +1396,26 @@ def generate(space, config: GenConfig | None = None, extents=None,
             def off_expr(j):
                 o = sum(sten[j][d] * st_[d] for d in range(s))
                 return f"base + ({o})" if o else "base"
+        if phase == "gather":
+            # pack=2: this query's u, coefficients, psi (and sub) go to outer variables
+            q = sctx["q"]
+            for d in range(s):
+                L(f"const {T} xf{d} = {f'xff{d}' if (intsel and not dyn) else f'({T})xc{d}'};")
+            for j in range(t.n):
+                if smem_fetch:
+                    L(f"const float c{j} = V[{off_expr(j)}];")
+                else:
+                    L(f"const float c{j} = __ldg(V + ({off_expr(j)}));")
+            us = emit_u_factory(L)("")
+            for d in range(s):
+                L(f"pu{q}{l}_{d} = {us[d]};")
+            for j in range(t.n):
+                L(f"pc{q}{l}_{j} = c{j};")
+            if t.K > 1:
+                L(f"ps{q}{l} = {t.psi[0] if t.uniform_psi else 'sg_psi[sub]'};")
+            if cfg.grad:
+                L(f"sb{q}{l} = sub;")
+            return
         # ---- local point u = T x_loc + t'
         if phase == "all":
             for d in range(s):
@@ -1555,6 +1674,187 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 em.indent = em.indent[:-2]
             L("}")
 
+    def emit_pack2_body():
+        """pack=2: two queries per thread.  Selection, fetch and u stay scalar per query
+        (in their own scopes); the polynomial evaluation runs once on float2 pairs, so
+        every FMA / add / mul of the (dominant) polynomial work is one FFMA2 / FADD2 /
+        FMUL2 for both queries."""
+        Bk = cfg.block
+        P_ = body.append
+        for q in "AB":
+            P_(f"  long long qo{q};")
+            for l in range(M):
+                P_("  float " + ", ".join(f"pu{q}{l}_{d}" for d in range(s)) + ";")
+                P_("  float " + ", ".join(f"pc{q}{l}_{j}" for j in range(t.n)) + ";")
+                if t.K > 1:
+                    P_(f"  int ps{q}{l};")
+                if cfg.grad:
+                    P_(f"  int sb{q}{l};")
+        for q, off in (("A", 0), ("B", Bk)):
+            P_(f"  {{  // query {q}")
+            if binned:
+                P_(f"    const int qv = qq + {off};")
+                P_("    const bool valid = qv < q_end;")
+                P_(f"    const float4 q4 = {ldf}(&sorted[valid ? qv : qq]);")
+                body.extend(binned_preamble("    "))
+            else:
+                P_(f"    const long long qraw = q0_ + threadIdx.x + {off};")
+                P_("    const bool valid = qraw < n;")
+                P_("    const long long qi = valid ? qraw : n - 1;")
+                body.extend(direct_preamble("    "))
+            P_(f"    qo{q} = valid ? qi : -1;")
+            sctx["q"] = q
+            for l in range(M):
+                em.lines = []
+                em.indent = "    "
+                em.line(f"{{  // coset {l}")
+                em.indent = "      "
+                emit_coset(l, False, phase="gather")
+                em.indent = "    "
+                em.line("}")
+                body.extend(em.lines)
+            P_("  }")
+        P_("  float accA = 0.f, accB = 0.f;")
+        if cfg.grad:
+            P_("  " + "; ".join(f"float gA{d} = 0.f, gB{d} = 0.f" for d in range(s)) + ";")
+        em.lines = []
+        em.indent = "  "
+        L = em.line
+
+        def neg2(x):
+            return f"make_float2(-({x}).x, -({x}).y)"
+
+        def pair_value(i, U, C, want_grad):
+            """(value pair, [grad pairs]) of reference polynomial i."""
+            f = symforms[i] if symforms is not None else None
+            if f is None:
+                if symforms is not None:
+                    node_list = [horner_factorize(space.ref_polys[i].poly)]
+                else:
+                    node_list = [tr for tr in trees[i] if tr is not None]
+                val = None
+                for nd in node_list:
+                    v = em.tree2(nd, U, C)
+                    if val is None:
+                        val = v
+                    else:
+                        nt = em.tmp("p")
+                        L(f"const float2 {nt} = __fadd2_rn({val}, {v});")
+                        val = nt
+                val = val or "make_float2(0.f, 0.f)"
+                gr = None
+                if want_grad:
+                    gr = [em.tree2(gtrees[i][a], U, C) if gtrees[i][a] is not None
+                          else "make_float2(0.f, 0.f)" for a in range(s)]
+                return val, gr
+            vv = []
+            for d in range(s):
+                if f.shift[d] != 0:
+                    nm = em.tmp("p")
+                    z = flit(-f.shift[d], F32)
+                    L(f"const float2 {nm} = __fadd2_rn({U[d]}, make_float2({z}, {z}));")
+                    vv.append(nm)
+                else:
+                    vv.append(U[d])
+            sv = [None] * len(f.mixes)
+            kk = len(f.axes)
+            for reps, syms in f.orbits:
+                if len(reps) == 1 << kk:
+                    x = {bits: C[j] for bits, j in reps}
+                    for tb in range(kk):
+                        nx = {}
+                        for b in x:
+                            if b >> tb & 1:
+                                continue
+                            hi_ = b | (1 << tb)
+                            a_, b_ = em.tmp("p"), em.tmp("p")
+                            L(f"const float2 {a_} = __fadd2_rn({x[b]}, {x[hi_]});")
+                            L(f"const float2 {b_} = __fadd2_rn({x[b]}, {neg2(x[hi_])});")
+                            nx[b], nx[hi_] = a_, b_
+                        x = nx
+                    for P, k_ in syms.items():
+                        sv[k_] = x[P]
+                else:
+                    for P, k_ in syms.items():
+                        expr = None
+                        for sign, j in f.mixes[k_]:
+                            term = C[j] if sign > 0 else neg2(C[j])
+                            if expr is None:
+                                expr = term
+                            else:
+                                nm = em.tmp("p")
+                                L(f"const float2 {nm} = __fadd2_rn({expr}, {term});")
+                                expr = nm
+                        sv[k_] = expr
+            val = em.tree2(sym_trees[i], vv, sv)
+            gr = None
+            if want_grad:
+                gr = [em.tree2(sym_gtrees[i][a], vv, sv) if sym_gtrees[i][a] is not None
+                      else "make_float2(0.f, 0.f)" for a in range(s)]
+            return val, gr
+
+        for l in range(M):
+            L(f"{{  // coset {l} (packed)")
+            U = []
+            for d in range(s):
+                L(f"const float2 U{d} = make_float2(puA{l}_{d}, puB{l}_{d});")
+                U.append(f"U{d}")
+            C = []
+            for j in range(t.n):
+                L(f"const float2 C{j} = make_float2(pcA{l}_{j}, pcB{l}_{j});")
+                C.append(f"C{j}")
+            psis = [0] if t.K == 1 else list(range(t.K))
+            dsum = {q: [None] * s for q in "AB"}
+            for i in psis:
+                val, gr = pair_value(i, U, C, cfg.grad)
+                for q, comp in (("A", "x"), ("B", "y")):
+                    if t.K == 1:
+                        L(f"acc{q} += ({val}).{comp};")
+                    else:
+                        L(f"acc{q} += (ps{q}{l} == {i}) ? ({val}).{comp} : 0.f;")
+                    if cfg.grad:
+                        for a in range(s):
+                            e = f"({gr[a]}).{comp}"
+                            if t.K > 1:
+                                e = f"((ps{q}{l} == {i}) ? {e} : 0.f)"
+                            dsum[q][a] = e if dsum[q][a] is None else f"{dsum[q][a]} + {e}"
+            if cfg.grad:
+                # grad_x += T_sub^T du per query
+                for q in "AB":
+                    du = []
+                    for a in range(s):
+                        nm = em.tmp("d")
+                        L(f"const float {nm} = {dsum[q][a]};")
+                        du.append(nm)
+                    for e in range(s):
+                        parts = []
+                        for a in range(s):
+                            if t.uniform_T:
+                                w = t.transforms[0][a][e]
+                                if w == 0:
+                                    continue
+                                parts.append(du[a] if w == 1 else (f"(-{du[a]})" if w == -1
+                                                                   else f"{flit(w, F32)} * {du[a]}"))
+                            elif tq:
+                                parts.append(f"sg_Tq[sb{q}{l} * 12 + {4 * a + e}] * {du[a]}")
+                            else:
+                                parts.append(f"sg_T[sb{q}{l} * {s * s} + {a * s + e}] * {du[a]}")
+                        if parts:
+                            L(f"g{q}{e} += {' + '.join(parts)};")
+            L("}")
+        body.extend(em.lines)
+        for q in "AB":
+            P_(f"  if (qo{q} >= 0) {{")
+            P_(f"    {stf}(&out[qo{q}], acc{q});")
+            if cfg.grad:
+                for d in range(s):
+                    P_(f"    {stf}(&grad[qo{q} * {s} + {d}], g{q}{d});")
+            P_("  }")
+        P_("  }")   # pair loop
+        if binned:
+            pass
+        P_("}")
+
     if sorted_:
         TQ, Bk = cfg.tile, cfg.block
         PQ = TQ // Bk
@@ -1703,6 +2003,8 @@ def generate(space, config: GenConfig | None = None, extents=None,
         body.append("}")
     elif sorted_:
         pass
+    elif pack2:
+        emit_pack2_body()
     elif M == 1:
         em.line("{")
         em.indent = "    "
@@ -1741,6 +2043,8 @@ def generate(space, config: GenConfig | None = None, extents=None,
         body.append(f"  {stf}(&rgba[qi], make_float4(C0, C1, C2, A));")
         body.append("  }")   # ray loop
         body.append("}")
+    elif pack2:
+        pass
     elif not sorted_:
         body += em.lines
         body.append(f"  {stf}(&out[qi], acc);")

@@ -37,11 +37,14 @@ def _xs(z, which, dtype=torch.float32):
 
 
 @pytest.mark.parametrize("name", golden_names())
-@pytest.mark.parametrize("mode", ["direct", "binned", "sorted", "direct_f64"])
+@pytest.mark.parametrize("mode", ["direct", "binned", "sorted", "direct_f64", "pack2", "pack2_binned"])
 def test_selection_bit_exact(name, mode):
     space, _, z, arrays = load_golden(name)
     if mode == "direct_f64":
         ev = _evaluator(space, arrays, dbg=True, select="f64")
+    elif mode.startswith("pack2"):
+        ev = _evaluator(space, arrays, dbg=True, pack=2,
+                        mode="binned" if mode.endswith("binned") else "direct")
     else:
         ev = _evaluator(space, arrays, dbg=True, mode=mode)
     for which in SETS:
@@ -73,6 +76,10 @@ CONFIGS = [
     dict(form="sym", mode="binned", params_mode="branchy"),
     dict(mode="sorted"),
     dict(select="f64"),
+    dict(pack=2),
+    dict(pack=2, mode="binned", form="sym"),
+    dict(pack=2, form="sites", params_md=(2, 4)),
+    dict(pack=2, mode="binned", block=256, select="f64"),
     dict(select="f64", mode="binned"),
     dict(select="f64", mode="sorted", form="sym"),
     dict(mode="sorted", form="sym", block=256, tile=512),
@@ -118,7 +125,8 @@ def test_values_f64_variant(name):
 
 
 @pytest.mark.parametrize("name", golden_names())
-@pytest.mark.parametrize("mode", ["direct", "binned", "table", "sym", "sorted", "sorted_sym"])
+@pytest.mark.parametrize("mode", ["direct", "binned", "table", "sym", "sorted", "sorted_sym",
+                                  "pack2", "pack2_binned_sym"])
 def test_gradient_vs_oracle(name, mode):
     space, ospace, z, arrays = load_golden(name)
     xs = z["uniform_xs"].astype(np.float64)
@@ -130,6 +138,10 @@ def test_gradient_vs_oracle(name, mode):
         ev = _evaluator(space, arrays, grad=True, form="sym")
     elif mode == "sorted_sym":
         ev = _evaluator(space, arrays, grad=True, form="sym", mode="sorted", block=256)
+    elif mode == "pack2":
+        ev = _evaluator(space, arrays, grad=True, pack=2)
+    elif mode == "pack2_binned_sym":
+        ev = _evaluator(space, arrays, grad=True, pack=2, mode="binned", form="sym")
     else:
         ev = _evaluator(space, arrays, grad=True, mode=mode)
     out, g, _ = ev(_xs(z, "uniform"))
@@ -139,10 +151,10 @@ def test_gradient_vs_oracle(name, mode):
 
 
 @pytest.mark.parametrize("name", golden_names())
-@pytest.mark.parametrize("mode", ["direct", "binned", "sorted"])
+@pytest.mark.parametrize("mode", ["direct", "binned", "sorted", "pack2"])
 def test_host_path_matches_device_path(name, mode):
     space, _, z, arrays = load_golden(name)
-    ev = _evaluator(space, arrays, mode=mode)
+    ev = _evaluator(space, arrays, pack=2) if mode == "pack2" else _evaluator(space, arrays, mode=mode)
     xs = z["uniform_xs"]
     dev = ev(torch.from_numpy(xs).cuda()).cpu().numpy()
     host = ev.eval_host(xs, chunk=257)

@@ -49,6 +49,13 @@ VARIANTS = {
     "sorted_b512_t2048": dict(mode="sorted", block=512, tile=2048),
     "sglobal": dict(sigma_smem=0),
     "nostream": dict(stream="default"),
+    "pack2": dict(pack=2),
+    "pack2_b128": dict(pack=2, block=128),
+    "pack2_b256": dict(pack=2, block=256),
+    "pack2_b512": dict(pack=2, block=512),
+    "pack2_b256_mb2": dict(pack=2, block=256, min_blocks=2),
+    "pack2_b128_mb4": dict(pack=2, block=128, min_blocks=4),
+    "pack2_imm": dict(pack=2, coeffs="imm"),
     "occ_128x8": dict(block=128, min_blocks=8),
     "occ_128x10": dict(block=128, min_blocks=10),
     "occ_256x4": dict(block=256, min_blocks=4),
