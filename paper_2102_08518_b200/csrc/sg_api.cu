@@ -388,16 +388,19 @@ __global__ void __launch_bounds__(THREADS) sg_bin_scatter_tiled(
   extern __shared__ __align__(16) unsigned char shb[];
   const int nb = (int)g.nbins;
   float4* tile = reinterpret_cast<float4*>(shb);                 // (4 * THREADS) records
-  int* tbin = reinterpret_cast<int*>(tile + (4 * THREADS));              // (4 * THREADS) bins
-  int* gpos = tbin + (4 * THREADS);                                      // nb: global cursor
+  int* tdst = reinterpret_cast<int*>(tile + (4 * THREADS));       // (4 * THREADS) destinations
+  int* gpos = tdst + (4 * THREADS);                                // nb: global cursor
   int* lcnt = gpos + nb;                                           // nb: tile counts
   int* loff = lcnt + nb;                                           // nb: tile offsets
+  int* gbase = loff + nb;                                          // nb: this tile's global base
   __shared__ int scan_sh[32];
   const int G = gridDim.x;
   for (int b = threadIdx.x; b < nb; b += blockDim.x) {
     const int c = mat[(long long)b * G + blockIdx.x];
     gpos[b] = c ? atomicAdd(&cursor[b], c) : 0;
+    lcnt[b] = 0;
   }
+  __syncthreads();
   const long long lo = (long long)blockIdx.x * per;
   const long long hi = min(n, lo + per);
   const bool vec = g.dim == 3 && ((((uintptr_t)xs) & 15) == 0);
@@ -422,8 +425,7 @@ __global__ void __launch_bounds__(THREADS) sg_bin_scatter_tiled(
         pc = __ldg(X4 + 2);
       }
     }
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) lcnt[b] = 0;
-    __syncthreads();
+    // (lcnt is zero here: cleared at allocation, then by phase B of the previous tile)
     // A: 4 consecutive queries per thread (one float4 triple when aligned)
     float4 rec[4];
     int bb[4], rk[4];
@@ -460,27 +462,26 @@ __global__ void __launch_bounds__(THREADS) sg_bin_scatter_tiled(
       for (int b = b0; b < b1; ++b) mine += lcnt[b];
       int at = sg_block_excl_scan(mine, scan_sh, nullptr);
       for (int b = b0; b < b1; ++b) {
+        const int c = lcnt[b];
         loff[b] = at;
-        at += lcnt[b];
+        gbase[b] = gpos[b];   // this tile's records of bin b start here in the output
+        gpos[b] += c;
+        lcnt[b] = 0;          // ready for the next tile's phase A
+        at += c;
       }
     }
     __syncthreads();
-    // C: place records bin-contiguously in the tile
+    // C: place records bin-contiguously in the tile, each with its final destination
 #pragma unroll
     for (int k = 0; k < 4; ++k)
       if (bb[k] >= 0) {
         const int slot = loff[bb[k]] + rk[k];
         tile[slot] = rec[k];
-        tbin[slot] = bb[k];
+        tdst[slot] = gbase[bb[k]] + rk[k];
       }
     __syncthreads();
     // D: coalesced runs to the global positions
-    for (int j = threadIdx.x; j < tn; j += blockDim.x) {
-      const int b = tbin[j];
-      sorted[gpos[b] + (j - loff[b])] = tile[j];
-    }
-    __syncthreads();
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) gpos[b] += lcnt[b];
+    for (int j = threadIdx.x; j < tn; j += blockDim.x) sorted[tdst[j]] = tile[j];
     __syncthreads();
   }
 }
@@ -927,11 +928,11 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
     cudaFuncSetAttribute(sg_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          SG_SMEM_BINS * sizeof(int));
     cudaFuncSetAttribute(sg_bin_scatter_tiled<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         4096 * (sizeof(float4) + sizeof(int)) + 3 * SG_TILED_MAX_BINS * sizeof(int));
+                         4096 * (sizeof(float4) + sizeof(int)) + 4 * SG_TILED_MAX_BINS * sizeof(int));
     cudaFuncSetAttribute(sg_bin_scatter_tiled<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         2048 * (sizeof(float4) + sizeof(int)) + 3 * SG_TILED_MAX_BINS * sizeof(int));
+                         2048 * (sizeof(float4) + sizeof(int)) + 4 * SG_TILED_MAX_BINS * sizeof(int));
     cudaFuncSetAttribute(sg_bin_scatter_tiled<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         1024 * (sizeof(float4) + sizeof(int)) + 3 * SG_TILED_MAX_BINS * sizeof(int));
+                         1024 * (sizeof(float4) + sizeof(int)) + 4 * SG_TILED_MAX_BINS * sizeof(int));
   });
   sg_bin_count<<<(unsigned)G, SG_SORT_THREADS, nb * sizeof(int), st>>>((const float*)xs, (long long)n,
                                                                       per, g, mat, bin_tot);
@@ -940,7 +941,7 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
                                   (int)max_items);
   CU(cudaGetLastError());
   if (nb <= (size_t)SG_TILED_MAX_BINS) {
-    const size_t shb = 4 * scatter_threads * (sizeof(float4) + sizeof(int)) + 3 * nb * sizeof(int);
+    const size_t shb = 4 * scatter_threads * (sizeof(float4) + sizeof(int)) + 4 * nb * sizeof(int);
     if (scatter_threads == 256)
       sg_bin_scatter_tiled<256><<<(unsigned)G, 256, shb, st>>>((const float*)xs, (long long)n, per,
                                                               g, mat, cursor, sorted);
