@@ -69,6 +69,7 @@ class GenConfig:
     select: str = "auto"         # selection arithmetic: "f64" | "int" (2^-30 fixed point) | "auto"
     sigma_smem: int = 4096       # sigma tables up to this many entries are staged in smem
     pack: int = 1                # 2: two queries per thread, polynomial FP in packed f32x2 (FFMA2)
+    prefetch: int = 0            # sorted: load the next pair's record + coefficients one iteration ahead
 
     def __post_init__(self):
         if self.float_width not in (F64, F32):
@@ -1434,16 +1435,20 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 L("const int psi = sg_psi[sub];")
         cvars = [f"c{j}" for j in range(t.n)]
 
+        def fetch_line(j, tag):
+            if phase == "eval" and sctx.get("prefetched"):
+                return f"const {T} c{j}{tag} = pfc{j};"     # loaded one iteration ahead
+            if smem_fetch:
+                return f"const {T} c{j}{tag} = V[{off_expr(j)}];"
+            return f"const {T} c{j}{tag} = __ldg(V + ({off_expr(j)}));"
+
         def run_plan_sym(psis, tag):
             """All fetches in plan order, then per psi the symmetry-mixed symbols and
             one Horner evaluation of psi'(v, s) (form "sym")."""
             for step in plan.steps:
                 if step.kind == FETCH:
                     j = step.index
-                    if smem_fetch:
-                        L(f"const {T} c{j}{tag} = V[{off_expr(j)}];")
-                    else:
-                        L(f"const {T} c{j}{tag} = __ldg(V + ({off_expr(j)}));")
+                    L(fetch_line(j, tag))
             u = emit_u(tag)
             accs, grads = {}, ({} if cfg.grad else None)
             for i in psis:
@@ -1507,10 +1512,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
             for step in plan.steps:
                 if step.kind == FETCH:
                     j = step.index
-                    if smem_fetch:
-                        L(f"const {T} c{j}{tag} = V[{off_expr(j)}];")
-                    else:
-                        L(f"const {T} c{j}{tag} = __ldg(V + ({off_expr(j)}));")
+                    L(fetch_line(j, tag))
                 elif step.kind == COMPUTE:
                     if u is None or refetch:
                         u = emit_u(f"{tag}_{nchunk}" if refetch else tag)
@@ -1599,10 +1601,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
             for step in plan.steps:
                 if step.kind == FETCH:
                     j = step.index
-                    if smem_fetch:
-                        L(f"const {T} c{j} = V[{off_expr(j)}];")
-                    else:
-                        L(f"const {T} c{j} = __ldg(V + ({off_expr(j)}));")
+                    L(fetch_line(j, ""))
                 elif step.kind == COMPUTE:
                     for j in plan.blocks[step.index]:
                         for q in range(nmp // w):
@@ -1919,15 +1918,56 @@ def generate(space, config: GenConfig | None = None, extents=None,
         body.append("    __syncthreads();")
         # phase 2: evaluate the pairs in psi order
         body.append("    const int tot = sg_tot;")
-        body.append(f"    for (int pos = threadIdx.x; pos < tot; pos += {Bk}) {{")
-        body.append("      const int e_ = sg_ord[pos];")
-        body.append("      const int pi_ = e_ & 0xffff;")
-        body.append("      const int sub = e_ >> 16;")
-        body.append("      const float4 rec = sg_rec[pi_];")
-        for d in range(s):
-            body.append(f"      const float u{d} = rec.{'xyz'[d]};")
-        body.append("      const int base = __float_as_int(rec.w);")
-        body.append(f"      const float* __restrict__ V = (const float*)vol.base[0];")
+        pf = cfg.prefetch and fetch_mode in ("table", "uniform")
+        sctx["prefetched"] = bool(pf)
+        if pf:
+            # software pipeline: pair pos + B's record, sub-region and coefficient gathers are
+            # issued before pair pos's polynomial, so the gathers' latency hides behind it
+            npad = t.n + 1 if t.n % 2 == 0 else t.n
+            sten = t.stencils[0]
+            st0 = strides[0]
+
+            def pf_load(pre, posv):
+                body.append(f"{pre}{{ const int e_ = sg_ord[{posv}];")
+                body.append(f"{pre}  nf_pi = e_ & 0xffff; nf_sub = e_ >> 16;")
+                body.append(f"{pre}  const float4 r_ = sg_rec[nf_pi];")
+                for d in range(s):
+                    body.append(f"{pre}  nf_u{d} = r_.{'xyz'[d]};")
+                body.append(f"{pre}  const int b_ = __float_as_int(r_.w);")
+                for j in range(t.n):
+                    if fetch_mode == "table":
+                        off = f"b_ + sg_off0[nf_sub * {npad} + {j}]"
+                    else:
+                        o = sum(sten[j][d] * st0[d] for d in range(s))
+                        off = f"b_ + ({o})"
+                    body.append(f"{pre}  nf_c{j} = __ldg((const float*)vol.base[0] + ({off}));")
+                body.append(f"{pre}}}")
+            body.append("    int nf_pi = 0, nf_sub = 0;")
+            body.append("    float " + ", ".join([f"nf_u{d} = 0.f" for d in range(s)]
+                                                + [f"nf_c{j} = 0.f" for j in range(t.n)]) + ";")
+            body.append("    if ((int)threadIdx.x < tot)")
+            pf_load("      ", "threadIdx.x")
+            body.append(f"    for (int pos = threadIdx.x; pos < tot; pos += {Bk}) {{")
+            body.append("      const int pi_ = nf_pi;")
+            body.append("      const int sub = nf_sub;")
+            for d in range(s):
+                body.append(f"      const float u{d} = nf_u{d};")
+            for j in range(t.n):
+                body.append(f"      const float pfc{j} = nf_c{j};")
+            body.append(f"      if (pos + {Bk} < tot)")
+            pf_load("        ", f"pos + {Bk}")
+            body.append(f"      const float* __restrict__ V = (const float*)vol.base[0];")
+            body.append("      const int base = 0;")
+        else:
+            body.append(f"    for (int pos = threadIdx.x; pos < tot; pos += {Bk}) {{")
+            body.append("      const int e_ = sg_ord[pos];")
+            body.append("      const int pi_ = e_ & 0xffff;")
+            body.append("      const int sub = e_ >> 16;")
+            body.append("      const float4 rec = sg_rec[pi_];")
+            for d in range(s):
+                body.append(f"      const float u{d} = rec.{'xyz'[d]};")
+            body.append("      const int base = __float_as_int(rec.w);")
+            body.append(f"      const float* __restrict__ V = (const float*)vol.base[0];")
         if t.K > 1:
             body.append(f"      const int psi = {psi_of('sub')};")
         body.append("      float acc = 0.0f;")

@@ -49,6 +49,9 @@ VARIANTS = {
     "sorted_b512_t2048": dict(mode="sorted", block=512, tile=2048),
     "sglobal": dict(sigma_smem=0),
     "nostream": dict(stream="default"),
+    "nopf": dict(prefetch=0),
+    "pf_b256_t1536": dict(mode="sorted", block=256, tile=1536),
+    "pf_b512_t1024": dict(mode="sorted", block=512, tile=1024),
     "pack2": dict(pack=2),
     "pack2_b128": dict(pack=2, block=128),
     "pack2_b256": dict(pack=2, block=256),
