@@ -1008,9 +1008,17 @@ static int launch(sg_module* m, const sg_volume* v, const void* xs, int64_t n, v
   long long grid = (nn + per_block - 1) / per_block;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device);
-  // grid-stride kernel: about four full waves, so per-CTA table staging is amortized;
-  // kernels with dynamic shared memory (sorted tiles) run one persistent wave
-  long long cap = (long long)sms * std::max(1, 2048 / m->info.block) * 4;
+  // grid-stride kernel: four waves of resident CTAs, so the per-CTA table staging is
+  // amortized over many queries; kernels with dynamic shared memory (sorted tiles) run
+  // one persistent wave
+  long long cap = (long long)sms * std::max(1, 2048 / m->info.block) * 2;
+  {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)m->kernel, m->info.block, 0) ==
+            cudaSuccess && occ > 0)
+      cap = (long long)sms * occ * 4;
+    cudaGetLastError();
+  }
   if (m->info.smem_bytes > 0) {
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)m->kernel, m->info.block,

@@ -774,7 +774,9 @@ def generate(space, config: GenConfig | None = None, extents=None,
             lit = ", ".join(flit(Fraction(v), F32) for v in vals)
         elif ctype == "double":
             lit = ", ".join(dlit(Fraction(v)) for v in vals)
-        A(f"__constant__ {ctype} {name}_c[{len(vals)}] = {{{lit}}};")
+        # global (not __constant__): the per-CTA staging copy reads thread-distinct addresses,
+        # which the constant cache serializes; coalesced __ldg reads do not
+        A(f"__device__ const {ctype} {name}_c[{len(vals)}] = {{{lit}}};")
 
     if sigma_global:
         A(f"__device__ const int sg_sigma_g[{len(t.sigma)}] = {{{', '.join(str(v) for v in t.sigma)}}};")
@@ -871,7 +873,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
         for name, ctype, vals in smem:
             B(f"  __shared__ __align__(16) {ctype} {name}[{len(vals)}];")
         for name, ctype, vals in smem:
-            B(f"  for (int i_ = threadIdx.x; i_ < {len(vals)}; i_ += {cfg.block}) {name}[i_] = {name}_c[i_];")
+            B(f"  for (int i_ = threadIdx.x; i_ < {len(vals)}; i_ += {cfg.block}) {name}[i_] = __ldg(&{name}_c[i_]);")
         if sorted_:
             TQ = cfg.tile
             MP = M * TQ
@@ -1015,7 +1017,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 addr = " + ".join(f"(lo{d} + {idx[d]}) * {gst[d]}" for d in range(s))
                 B(f"      sg_brick[{l * brick_elems} + e_] = __ldg(G + {addr}); }} }}")
         for name, ctype, vals in smem:
-            B(f"  for (int i_ = threadIdx.x; i_ < {len(vals)}; i_ += {cfg.block}) {name}[i_] = {name}_c[i_];")
+            B(f"  for (int i_ = threadIdx.x; i_ < {len(vals)}; i_ += {cfg.block}) {name}[i_] = __ldg(&{name}_c[i_]);")
         B("  __syncthreads();")
         if cfg.stage == "tma" and smem_fetch:
             B('  asm volatile("{\\n .reg .pred p;\\n SG_WAIT_%=:\\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\\n @!p bra SG_WAIT_%=;\\n}" :: "r"(sg_bar_a) : "memory");')
