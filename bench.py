@@ -398,6 +398,24 @@ def run_ours(args, rank, world, device):
     value = total_q / (ms / 1e3) / 1e9
     kernel_ms = ms / args.steps
 
+    gather_ms = None
+    if args.gather and world > 1:
+        # optional: every rank receives all ranks' results (reported beside, not inside, value)
+        from paper_2102_08518_b200.dist import gather_results
+        total = c["queries"] if c["scaling"] == "strong" else n * world
+        gather_results(out, total, device=device)
+        torch.cuda.synchronize(device)
+        dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        gather_results(out, total, device=device)
+        g1.record(stream)
+        torch.cuda.synchronize(device)
+        gather_ms = float(torch.tensor([g0.elapsed_time(g1)], dtype=torch.float64, device=device).item())
+        gt = torch.tensor([gather_ms], dtype=torch.float64, device=device)
+        dist.all_reduce(gt, op=dist.ReduceOp.MAX)
+        gather_ms = float(gt.item())
+
     # ---- end to end through the C-ABI host path (pinned buffers)
     xs_host = xs.cpu().pin_memory()
     out_host = torch.empty(n, dtype=torch.float32).pin_memory()
@@ -458,6 +476,7 @@ def run_ours(args, rank, world, device):
                    "form": prog.config.form, "coeffs": prog.config.coeffs, "mode": prog.mode,
                    "bin": prog.bin, "brick": list(prog.brick), "block": prog.block,
                    "eval_kernel_ms": round(eval_kernel_ms, 4), "wall_s": round(t_wall, 3)},
+        "gather_ms": gather_ms,
         "gpu_launches_note": "per step: query sort (sg_bin_count, sg_bin_plan, sg_bin_scatter_tiled) "
                              "+ sg_eval_kernel" if prog.mode == "binned" else "1 kernel per step",
     }
@@ -653,6 +672,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--gather", action="store_true",
+                    help="also time the optional result gather to every rank (all_gather over "
+                         "NCCL/NVLink, SURVEY 8e), reported separately as gather_ms")
     args = ap.parse_args()
     args.config = args.config or default_config_name()
     args.warmup = max(3, args.warmup)

@@ -91,10 +91,11 @@ def test_multi_rank_bench_code_path():
     env = dict(os.environ, SPLINEGPU_DIST_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29533", "bench.py", "--gpus", "2",
-           "--config", "c1", "--steps", "3", "--warmup", "3", "--no-cpu"]
+           "--config", "c1", "--steps", "3", "--warmup", "3", "--no-cpu", "--gather"]
     r = subprocess.run(cmd, cwd=str(bench.ROOT), env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["parallelism"].startswith("query shards x2")
+    assert d["gather_ms"] is not None and d["gather_ms"] > 0
