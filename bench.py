@@ -596,7 +596,7 @@ def run_reference(args, rank, world):
     if c["kind"] == "render":
         return run_reference_render(args, c, space, arrays)
     xs = make_queries(args.config, 0, 1 << 18, "cpu").numpy()
-    total_budget = 150.0                       # seconds for the whole --steps/--warmup run
+    total_budget = 10.0 * args.cpu_budget       # seconds for the whole run (default 150 s)
     per_step = total_budget / (args.steps + args.warmup)
     cores = len(os.sched_getaffinity(0))
     shard = 1 << 11
