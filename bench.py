@@ -51,7 +51,7 @@ CONFIGS = {
                desc="BCC quintic box spline (4 dirs x2), 2x101^3 coset-split, 2^24 uniform"),
     "c3": dict(space="bcc_voronoi2", extents=(203, 203, 203), queries=1 << 26, kind="rays",
                rays=(512, 512, 256), grad=False, scaling="weak",
-               variant=dict(mode="sorted", coeffs="imm", block=512),
+               variant=dict(mode="sorted", coeffs="imm", block=512, radix=1),
                desc="BCC Voronoi spline (order 2, piecewise cubic), 2x203^3, 2^26 ray-ordered"),
     "c4": dict(space="fcc_box6", extents=(161, 161, 161), queries=1 << 26, kind="uniform",
                grad=True, scaling="weak", variant=dict(mode="direct", coeffs="imm", block=128),
@@ -68,7 +68,7 @@ CONFIGS = {
                  desc="c3r with gradient (Lambert) shading at every sample"),
     "c5": dict(space="bcc_voronoi2", extents=(406, 406, 406), queries=1 << 30, kind="rays",
                rays=(1024, 1024, 1024), grad=False, scaling="strong",
-               variant=dict(mode="sorted", coeffs="imm", block=512),
+               variant=dict(mode="sorted", coeffs="imm", block=512, radix=1),
                desc="BCC Voronoi spline (order 2), 2x406^3, 2^30 ray-ordered sharded over the GPUs"),
 }
 DEFAULT_CONFIG = "c2"

@@ -70,6 +70,7 @@ class GenConfig:
     sigma_smem: int = 4096       # sigma tables up to this many entries are staged in smem
     pack: int = 1                # 2: two queries per thread, polynomial FP in packed f32x2 (FFMA2)
     prefetch: int = 0            # sorted: load the next pair's record + coefficients one iteration ahead
+    radix: int = 0               # 1: sub-region via a mixed-radix index of the plane-family counts
 
     def __post_init__(self):
         if self.float_width not in (F64, F32):
@@ -691,7 +692,31 @@ def generate(space, config: GenConfig | None = None, extents=None,
     smem = []     # (name, ctype, values)
     use_sigma = t.nsub > 1 and len(space.planes) > 0 and len(set(t.sigma)) > 1
     sigma_global = use_sigma and len(t.sigma) > cfg.sigma_smem
-    if use_sigma and not sigma_global:
+    families = plane_families(t)
+    # radix: when every plane belongs to a threshold family, the family counts (c_f in
+    # 0..r_f) index a table directly -- sub = sigma[(sum_f ((1 << c_f) - 1) << b0_f) mod p]
+    # is precomputed for every count combination, so no bit assembly and no modulo remain
+    radix = None
+    tab_r = []
+    if cfg.radix and use_sigma and families:
+        fam_planes = sum(r for (_b0, r, _sc, _m1) in families.values())
+        combos = 1
+        for (_b0, r, _sc, _m1) in families.values():
+            combos *= r + 1
+        if fam_planes == len(t.planes) and combos <= (1 << 18):
+            fl = sorted(families.items(), key=lambda kv: kv[1][0])
+            strides_r, acc_ = {}, 1
+            for nrm, (b0, r, sc, m1) in reversed(fl):
+                strides_r[nrm] = acc_
+                acc_ *= r + 1
+            for idx in range(combos):
+                q, rem = 0, idx
+                for nrm, (b0, r, sc, m1) in fl:
+                    c_ = (rem // strides_r[nrm]) % (r + 1)
+                    q |= ((1 << c_) - 1) << b0
+                tab_r.append(t.sigma[q % t.modulus] if (t.compress or q < len(t.sigma)) else -1)
+            radix = strides_r
+    if use_sigma and not sigma_global and radix is None:
         smem.append(("sg_sigma", "short" if _sigma_short(t) else "int", list(t.sigma)))
     tq = s == 3 and fw == F32 and not (t.uniform_T and t.uniform_tp)
     if tq:
@@ -778,7 +803,9 @@ def generate(space, config: GenConfig | None = None, extents=None,
         # which the constant cache serializes; coalesced __ldg reads do not
         A(f"__device__ const {ctype} {name}_c[{len(vals)}] = {{{lit}}};")
 
-    if sigma_global:
+    if radix is not None:
+        A(f"__device__ const short sg_sigma_r[{len(tab_r)}] = {{{', '.join(str(v) for v in tab_r)}}};")
+    if sigma_global and radix is None:
         A(f"__device__ const int sg_sigma_g[{len(t.sigma)}] = {{{', '.join(str(v) for v in t.sigma)}}};")
 
     # ---- kernel -------------------------------------------------------------
@@ -1158,7 +1185,10 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 cnt = em.tmp("cnt")
                 arg = f"({dv} >> {sh}) - ({m1 - 1})" if m1 != 1 else f"{dv} >> {sh}"
                 L(f"const int {cnt} = min(max({arg}, 0), {r});")
-                L(f"qq |= ((1u << {cnt}) - 1u) << {b0};")
+                if radix is not None:
+                    L(f"qq += (unsigned)({cnt} * {radix[nrm]});")
+                else:
+                    L(f"qq |= ((1u << {cnt}) - 1u) << {b0};")
                 continue
             D = int(off * 2 ** FIX)
             L(f"qq |= ({idot(nrm)} >= {D}) ? {1 << i}u : 0u;")
@@ -1271,7 +1301,10 @@ def generate(space, config: GenConfig | None = None, extents=None,
                     b0, r, sc, m1 = counted[nrm]
                     cnt = em.tmp("cnt")
                     L(f"const int {cnt} = min(max(__double2int_rd(({acc or '0.0'}) * {float(sc)!r}) - ({m1 - 1}), 0), {r});")
-                    L(f"q |= ((1u << {cnt}) - 1u) << {b0};")
+                    if radix is not None:
+                        L(f"q += (unsigned)({cnt} * {radix[nrm]});")
+                    else:
+                        L(f"q |= ((1u << {cnt}) - 1u) << {b0};")
                     continue
                 nz = [(e, w) for e, w in enumerate(nrm) if w != 0]
                 if off == 0 and len(nz) == 2 and all(abs(w) == 1 for _, w in nz):
@@ -1310,9 +1343,13 @@ def generate(space, config: GenConfig | None = None, extents=None,
             if space.planes:
                 L("unsigned q = qq;")
         if space.planes:
-            if t.compress:
+            if radix is not None:
+                L("int sub = __ldg(&sg_sigma_r[q]);")
+            elif t.compress:
                 L(f"q = q % {P}u;")
-            if sigma_global:
+            if radix is not None:
+                pass
+            elif sigma_global:
                 L("int sub = __ldg(&sg_sigma_g[q]);")
             elif use_sigma:
                 L("int sub = sg_sigma[q];")

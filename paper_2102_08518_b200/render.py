@@ -38,11 +38,12 @@ def render_config(space: SplineSpace, shade: bool = False, **variant) -> GenConf
     """The renderer's kernel variant.  One ray per thread (predicated dispatch, immediates,
     128-thread CTAs) for single-polynomial spaces; for K > 1 reference polynomials the
     samples of 128 rays x (tile / 128) steps are sorted by psi in shared memory first
-    (measured on B200: BCC Voronoi 2.75 -> 2.25 ms per 512 x 512 x 256 image)."""
+    (measured on B200: BCC Voronoi 2.75 -> 2.18 ms per 512 x 512 x 256 image)."""
     kw = dict(params=ScheduleParams(1, space.stencil_size, "predicated"), mode="render",
               grad=shade, block=128)
     if len(space.ref_polys) > 1:
         kw.update(block=256, tile=1024) if shade else kw.update(block=512, tile=1536)
+        kw.update(radix=1)   # sub-region from the plane-family counts when they cover every plane
     kw.update(variant)
     return GenConfig(**kw)
 

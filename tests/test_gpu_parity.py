@@ -37,11 +37,15 @@ def _xs(z, which, dtype=torch.float32):
 
 
 @pytest.mark.parametrize("name", golden_names())
-@pytest.mark.parametrize("mode", ["direct", "binned", "sorted", "direct_f64", "pack2", "pack2_binned"])
+@pytest.mark.parametrize("mode", ["direct", "binned", "sorted", "direct_f64", "pack2", "pack2_binned",
+                                  "radix", "radix_f64"])
 def test_selection_bit_exact(name, mode):
     space, _, z, arrays = load_golden(name)
     if mode == "direct_f64":
         ev = _evaluator(space, arrays, dbg=True, select="f64")
+    elif mode.startswith("radix"):
+        ev = _evaluator(space, arrays, dbg=True, radix=1, mode="sorted",
+                        select="f64" if mode.endswith("f64") else "auto")
     elif mode.startswith("pack2"):
         ev = _evaluator(space, arrays, dbg=True, pack=2,
                         mode="binned" if mode.endswith("binned") else "direct")
@@ -77,6 +81,8 @@ CONFIGS = [
     dict(mode="sorted"),
     dict(select="f64"),
     dict(pack=2),
+    dict(radix=1),
+    dict(radix=1, mode="sorted", select="f64"),
     dict(pack=2, mode="binned", form="sym"),
     dict(pack=2, form="sites", params_md=(2, 4)),
     dict(pack=2, mode="binned", block=256, select="f64"),

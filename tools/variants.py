@@ -25,6 +25,8 @@ RENDER_VARIANTS = {
     "sorted_b256_t1536": dict(block=256, tile=1536),
     "sorted_b256_t1024": dict(block=256, tile=1024),
     "sorted_b512_t1536": dict(block=512, tile=1536),
+    "sorted_b512_t1536_radix": dict(block=512, tile=1536, radix=1),
+    "sorted_b256_t1024_radix": dict(block=256, tile=1024, radix=1),
     "sorted_b512_t2048": dict(block=512, tile=2048),
     "sorted_b128_t1024": dict(block=128, tile=1024),
     "sorted_b384_t1536": dict(block=384, tile=1536),
@@ -50,6 +52,8 @@ VARIANTS = {
     "sglobal": dict(sigma_smem=0),
     "nostream": dict(stream="default"),
     "nopf": dict(prefetch=0),
+    "radix": dict(radix=1),
+    "radix_direct": dict(radix=1, mode="direct", block=128),
     "pf_b256_t1536": dict(mode="sorted", block=256, tile=1536),
     "pf_b512_t1024": dict(mode="sorted", block=512, tile=1024),
     "pack2": dict(pack=2),
