@@ -71,6 +71,7 @@ class GenConfig:
     pack: int = 1                # 2: two queries per thread, polynomial FP in packed f32x2 (FFMA2)
     prefetch: int = 0            # sorted: load the next pair's record + coefficients one iteration ahead
     radix: int = 0               # 1: sub-region via a mixed-radix index of the plane-family counts
+    rank: str = "match"          # sorted: rank in the psi class by "match" (warp-aggregated) | "atomic"
 
     def __post_init__(self):
         if self.float_width not in (F64, F32):
@@ -1080,6 +1081,11 @@ def generate(space, config: GenConfig | None = None, extents=None,
             L("const int psi_ = 0;")
         L(f"sg_rec[{l * sctx['TQ']} + ql] = make_float4({us[0]}, {us[1]}, {us[2]}, "
           f"__int_as_float(base + coff{l}));")
+        if cfg.rank == "atomic":
+            # one shared-memory atomic per pair (same-class lanes serialize in the unit)
+            L(f"const int rk_ = valid ? atomicAdd(&sg_cnt[psi_], 1) : 0;")
+            L(f"sg_key[{l * sctx['TQ']} + ql] = valid ? (rk_ | (sub << 16)) : -1;")
+            return
         L(f"const int kp_ = valid ? psi_ : {t.K};")
         L("const unsigned mm_ = __match_any_sync(0xffffffffu, kp_);")
         L("const int ld_ = __ffs(mm_) - 1;")

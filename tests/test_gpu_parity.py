@@ -83,6 +83,7 @@ CONFIGS = [
     dict(pack=2),
     dict(radix=1),
     dict(radix=1, mode="sorted", select="f64"),
+    dict(mode="sorted", rank="atomic", radix=1),
     dict(pack=2, mode="binned", form="sym"),
     dict(pack=2, form="sites", params_md=(2, 4)),
     dict(pack=2, mode="binned", block=256, select="f64"),

@@ -26,6 +26,7 @@ RENDER_VARIANTS = {
     "sorted_b256_t1024": dict(block=256, tile=1024),
     "sorted_b512_t1536": dict(block=512, tile=1536),
     "sorted_b512_t1536_radix": dict(block=512, tile=1536, radix=1),
+    "sorted_b512_t1536_radix_atomic": dict(block=512, tile=1536, radix=1, rank="atomic"),
     "sorted_b256_t1024_radix": dict(block=256, tile=1024, radix=1),
     "sorted_b512_t2048": dict(block=512, tile=2048),
     "sorted_b128_t1024": dict(block=128, tile=1024),
@@ -53,6 +54,7 @@ VARIANTS = {
     "nostream": dict(stream="default"),
     "nopf": dict(prefetch=0),
     "radix": dict(radix=1),
+    "rank_atomic": dict(rank="atomic"),
     "radix_direct": dict(radix=1, mode="direct", block=128),
     "pf_b256_t1536": dict(mode="sorted", block=256, tile=1536),
     "pf_b512_t1024": dict(mode="sorted", block=512, tile=1024),
