@@ -480,7 +480,7 @@ def run_ours(args, rank, world, device):
         "gpu_launches_note": "per step: query sort (sg_bin_count, sg_bin_plan, sg_bin_scatter_tiled) "
                              "+ sg_eval_kernel" if prog.mode == "binned" else "1 kernel per step",
     }
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1:   # the CPU baseline is an N = 1 figure
         xs_np = xs[: 1 << 20].cpu().numpy()
         line["cpu_baseline"] = cpu_baseline(c["space"], arrays, xs_np, budget_s=args.cpu_budget,
                                             shard=1 << 12)
@@ -565,7 +565,7 @@ def run_render(args, rank, world, device):
         "clocks": clk.summary(),
         "kernel": {"regs": r.ev.module.regs()[0], "mode": "render", "block": r.prog.block},
     }
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1:
         from oracle import refeval
         from oracle import render as orender
         from paper_2102_08518_b200.model import SPACES_DIR
