@@ -53,6 +53,14 @@ VARIANTS = {
     "sglobal": dict(sigma_smem=0),
     "nostream": dict(stream="default"),
     "nopf": dict(prefetch=0),
+    "bin_b256": dict(mode="binned", block=256),
+    "bin_b1024": dict(mode="binned", block=1024),
+    "bin_b384": dict(mode="binned", block=384),
+    "bin_b640": dict(mode="binned", block=640),
+    "bin_b512_mb2": dict(mode="binned", block=512, min_blocks=2),
+    "binned_l1": dict(mode="binned", stage="l1", block=256),
+    "binned_l1_b128": dict(mode="binned", stage="l1", block=128, bin=8),
+    "binned_tma": dict(mode="binned", block=256),
     "radix": dict(radix=1),
     "rank_atomic": dict(rank="atomic"),
     "radix_direct": dict(radix=1, mode="direct", block=128),
