@@ -381,15 +381,16 @@ __global__ void __launch_bounds__(SG_SORT_THREADS) sg_bin_scatter(
 constexpr int SG_TILE = 4096;   // records per tile of the 1024-thread instantiation
 constexpr int SG_TILED_MAX_BINS = 2048;   // per-tile histogram cost grows with the bin count
 
-template <int THREADS>
+template <int THREADS, int GROUPS>
 __global__ void __launch_bounds__(THREADS) sg_bin_scatter_tiled(
     const float* __restrict__ xs, long long n, long long per, BinGeom g,
     const int* __restrict__ mat, int* __restrict__ cursor, float4* __restrict__ sorted) {
+  constexpr int TILE = 4 * THREADS * GROUPS;   // records per tile: GROUPS x 4 per thread
   extern __shared__ __align__(16) unsigned char shb[];
   const int nb = (int)g.nbins;
-  float4* tile = reinterpret_cast<float4*>(shb);                 // (4 * THREADS) records
-  int* tdst = reinterpret_cast<int*>(tile + (4 * THREADS));       // (4 * THREADS) destinations
-  int* gpos = tdst + (4 * THREADS);                                // nb: global cursor
+  float4* tile = reinterpret_cast<float4*>(shb);                 // TILE records
+  int* tdst = reinterpret_cast<int*>(tile + TILE);                // TILE destinations
+  int* gpos = tdst + TILE;                                         // nb: global cursor
   int* lcnt = gpos + nb;                                           // nb: tile counts
   int* loff = lcnt + nb;                                           // nb: tile offsets
   int* gbase = loff + nb;                                          // nb: this tile's global base
@@ -404,57 +405,65 @@ __global__ void __launch_bounds__(THREADS) sg_bin_scatter_tiled(
   const long long lo = (long long)blockIdx.x * per;
   const long long hi = min(n, lo + per);
   const bool vec = g.dim == 3 && ((((uintptr_t)xs) & 15) == 0);
-  const int q0 = threadIdx.x * 4;
-  // software pipeline: the next tile's query triple is loaded while this tile is sorted
-  float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pb = pa, pc = pa;
-  if (vec && lo + q0 + 4 <= hi) {
-    const float4* X4 = reinterpret_cast<const float4*>(xs + (lo + q0) * 3);
-    pa = X4[0];
-    pb = X4[1];
-    pc = X4[2];
-  }
-  for (long long t0 = lo; t0 < hi; t0 += (4 * THREADS)) {
-    const int tn = (int)min((long long)(4 * THREADS), hi - t0);
-    const float4 ca = pa, cb = pb, cc = pc;
-    {
-      const long long nx = t0 + (4 * THREADS) + q0;
-      if (vec && nx + 4 <= hi) {
-        const float4* X4 = reinterpret_cast<const float4*>(xs + nx * 3);
-        pa = __ldg(X4);
-        pb = __ldg(X4 + 1);
-        pc = __ldg(X4 + 2);
-      }
+  // software pipeline: the next tile's query triples are loaded while this tile is sorted
+  float4 pa[GROUPS], pb[GROUPS], pc[GROUPS];
+#pragma unroll
+  for (int gi = 0; gi < GROUPS; ++gi) {
+    pa[gi] = pb[gi] = pc[gi] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const long long q = lo + gi * 4 * THREADS + threadIdx.x * 4;
+    if (vec && q + 4 <= hi) {
+      const float4* X4 = reinterpret_cast<const float4*>(xs + q * 3);
+      pa[gi] = X4[0];
+      pb[gi] = X4[1];
+      pc[gi] = X4[2];
     }
-    // (lcnt is zero here: cleared at allocation, then by phase B of the previous tile)
-    // A: 4 consecutive queries per thread (one float4 triple when aligned)
-    float4 rec[4];
-    int bb[4], rk[4];
+  }
+  for (long long t0 = lo; t0 < hi; t0 += TILE) {
+    const int tn = (int)min((long long)TILE, hi - t0);
+    float4 rec[4 * GROUPS];
+    int bb[4 * GROUPS], rk[4 * GROUPS];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) bb[k] = -1;
-    if (q0 < tn) {
-      const long long i0 = t0 + q0;
-      if (vec && q0 + 4 <= tn) {
-        const float4 a = ca, b = cb, c = cc;
-        rec[0] = make_float4(a.x, a.y, a.z, __int_as_float((int)i0));
-        rec[1] = make_float4(a.w, b.x, b.y, __int_as_float((int)(i0 + 1)));
-        rec[2] = make_float4(b.z, b.w, c.x, __int_as_float((int)(i0 + 2)));
-        rec[3] = make_float4(c.y, c.z, c.w, __int_as_float((int)(i0 + 3)));
+    for (int gi = 0; gi < GROUPS; ++gi) {
+      const int q0 = gi * 4 * THREADS + threadIdx.x * 4;
+      const float4 ca = pa[gi], cb = pb[gi], cc = pc[gi];
+      {
+        const long long nx = t0 + TILE + q0;
+        if (vec && nx + 4 <= hi) {
+          const float4* X4 = reinterpret_cast<const float4*>(xs + nx * 3);
+          pa[gi] = __ldg(X4);
+          pb[gi] = __ldg(X4 + 1);
+          pc[gi] = __ldg(X4 + 2);
+        }
+      }
+      // A: 4 consecutive queries per thread and group (one float4 triple when aligned)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) bb[k] = sg_bin_xyz(rec[k].x, rec[k].y, rec[k].z, g);
-      } else {
-        for (int k = 0; k < 4 && q0 + k < tn; ++k) {
-          const long long i = i0 + k;
-          rec[k] = make_float4(xs[i * g.dim], g.dim > 1 ? xs[i * g.dim + 1] : 0.f,
-                               g.dim > 2 ? xs[i * g.dim + 2] : 0.f, __int_as_float((int)i));
-          bb[k] = sg_bin_xyz(rec[k].x, rec[k].y, rec[k].z, g);
+      for (int k = 0; k < 4; ++k) bb[4 * gi + k] = -1;
+      if (q0 < tn) {
+        const long long i0 = t0 + q0;
+        if (vec && q0 + 4 <= tn) {
+          rec[4 * gi + 0] = make_float4(ca.x, ca.y, ca.z, __int_as_float((int)i0));
+          rec[4 * gi + 1] = make_float4(ca.w, cb.x, cb.y, __int_as_float((int)(i0 + 1)));
+          rec[4 * gi + 2] = make_float4(cb.z, cb.w, cc.x, __int_as_float((int)(i0 + 2)));
+          rec[4 * gi + 3] = make_float4(cc.y, cc.z, cc.w, __int_as_float((int)(i0 + 3)));
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            bb[4 * gi + k] = sg_bin_xyz(rec[4 * gi + k].x, rec[4 * gi + k].y, rec[4 * gi + k].z, g);
+        } else {
+          for (int k = 0; k < 4 && q0 + k < tn; ++k) {
+            const long long i = i0 + k;
+            rec[4 * gi + k] = make_float4(xs[i * g.dim], g.dim > 1 ? xs[i * g.dim + 1] : 0.f,
+                                          g.dim > 2 ? xs[i * g.dim + 2] : 0.f, __int_as_float((int)i));
+            bb[4 * gi + k] = sg_bin_xyz(rec[4 * gi + k].x, rec[4 * gi + k].y, rec[4 * gi + k].z, g);
+          }
         }
       }
     }
+    // (lcnt is zero here: cleared at start, then by phase B of the previous tile)
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+    for (int k = 0; k < 4 * GROUPS; ++k)
       if (bb[k] >= 0) rk[k] = atomicAdd(&lcnt[bb[k]], 1);
     __syncthreads();
-    // B: tile offsets (exclusive scan over bins)
+    // B: tile offsets (exclusive scan over bins), this tile's global bases, counts reset
     {
       const int per_t = (nb + THREADS - 1) / THREADS;
       const int b0 = threadIdx.x * per_t, b1 = min(nb, b0 + per_t);
@@ -473,7 +482,7 @@ __global__ void __launch_bounds__(THREADS) sg_bin_scatter_tiled(
     __syncthreads();
     // C: place records bin-contiguously in the tile, each with its final destination
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+    for (int k = 0; k < 4 * GROUPS; ++k)
       if (bb[k] >= 0) {
         const int slot = loff[bb[k]] + rk[k];
         tile[slot] = rec[k];
@@ -889,6 +898,13 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
   // tiles, short ones with 1024-thread tiles (fewer barriers per query)
   const int scatter_threads = scatter_threads_env ? scatter_threads_env
                                                   : ((n + G - 1) / G >= 32768 ? 512 : 1024);
+  static const int scatter_groups_env = [] {   // queries per thread / 4 (env SPLINEGPU_SCATTER_GROUPS)
+    const char* e = getenv("SPLINEGPU_SCATTER_GROUPS");
+    return e ? atoi(e) : 0;
+  }();
+  int scatter_groups = scatter_groups_env > 0 ? scatter_groups_env : 1;
+  if (!((scatter_threads == 512 && scatter_groups == 2) || (scatter_threads == 256 && scatter_groups == 4)))
+    scatter_groups = 1;
   const long long per = ((n + G - 1) / G + 3) & ~3LL;   // multiple of 4: float4 query groups
   const long long mlen = (long long)nb * G;
   const int chunk = std::max(32, in.chunk);
@@ -927,12 +943,17 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
                          2 * SG_SMEM_BINS * sizeof(int));
     cudaFuncSetAttribute(sg_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          SG_SMEM_BINS * sizeof(int));
-    cudaFuncSetAttribute(sg_bin_scatter_tiled<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         4096 * (sizeof(float4) + sizeof(int)) + 4 * SG_TILED_MAX_BINS * sizeof(int));
-    cudaFuncSetAttribute(sg_bin_scatter_tiled<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         2048 * (sizeof(float4) + sizeof(int)) + 4 * SG_TILED_MAX_BINS * sizeof(int));
-    cudaFuncSetAttribute(sg_bin_scatter_tiled<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         1024 * (sizeof(float4) + sizeof(int)) + 4 * SG_TILED_MAX_BINS * sizeof(int));
+    const int tb = 4 * SG_TILED_MAX_BINS * sizeof(int);
+    cudaFuncSetAttribute(sg_bin_scatter_tiled<1024, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         4096 * (sizeof(float4) + sizeof(int)) + tb);
+    cudaFuncSetAttribute(sg_bin_scatter_tiled<512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         2048 * (sizeof(float4) + sizeof(int)) + tb);
+    cudaFuncSetAttribute(sg_bin_scatter_tiled<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         4096 * (sizeof(float4) + sizeof(int)) + tb);
+    cudaFuncSetAttribute(sg_bin_scatter_tiled<256, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         1024 * (sizeof(float4) + sizeof(int)) + tb);
+    cudaFuncSetAttribute(sg_bin_scatter_tiled<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         4096 * (sizeof(float4) + sizeof(int)) + tb);
   });
   sg_bin_count<<<(unsigned)G, SG_SORT_THREADS, nb * sizeof(int), st>>>((const float*)xs, (long long)n,
                                                                       per, g, mat, bin_tot);
@@ -941,16 +962,19 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
                                   (int)max_items);
   CU(cudaGetLastError());
   if (nb <= (size_t)SG_TILED_MAX_BINS) {
-    const size_t shb = 4 * scatter_threads * (sizeof(float4) + sizeof(int)) + 4 * nb * sizeof(int);
-    if (scatter_threads == 256)
-      sg_bin_scatter_tiled<256><<<(unsigned)G, 256, shb, st>>>((const float*)xs, (long long)n, per,
-                                                              g, mat, cursor, sorted);
+    const size_t shb = 4 * scatter_threads * scatter_groups * (sizeof(float4) + sizeof(int)) +
+                       4 * nb * sizeof(int);
+    const float* xq = (const float*)xs;
+    if (scatter_threads == 256 && scatter_groups == 4)
+      sg_bin_scatter_tiled<256, 4><<<(unsigned)G, 256, shb, st>>>(xq, (long long)n, per, g, mat, cursor, sorted);
+    else if (scatter_threads == 256)
+      sg_bin_scatter_tiled<256, 1><<<(unsigned)G, 256, shb, st>>>(xq, (long long)n, per, g, mat, cursor, sorted);
+    else if (scatter_threads == 512 && scatter_groups == 2)
+      sg_bin_scatter_tiled<512, 2><<<(unsigned)G, 512, shb, st>>>(xq, (long long)n, per, g, mat, cursor, sorted);
     else if (scatter_threads == 512)
-      sg_bin_scatter_tiled<512><<<(unsigned)G, 512, shb, st>>>((const float*)xs, (long long)n, per,
-                                                              g, mat, cursor, sorted);
+      sg_bin_scatter_tiled<512, 1><<<(unsigned)G, 512, shb, st>>>(xq, (long long)n, per, g, mat, cursor, sorted);
     else
-      sg_bin_scatter_tiled<1024><<<(unsigned)G, 1024, shb, st>>>((const float*)xs, (long long)n,
-                                                                per, g, mat, cursor, sorted);
+      sg_bin_scatter_tiled<1024, 1><<<(unsigned)G, 1024, shb, st>>>(xq, (long long)n, per, g, mat, cursor, sorted);
   } else {
     sg_bin_scatter<<<(unsigned)G, SG_SORT_THREADS, nb * sizeof(int), st>>>(
         (const float*)xs, (long long)n, per, g, mat, cursor, sorted);

@@ -59,6 +59,10 @@ VARIANTS = {
     "bin_b640": dict(mode="binned", block=640),
     "bin_b512_mb2": dict(mode="binned", block=512, min_blocks=2),
     "binned_l1": dict(mode="binned", stage="l1", block=256),
+    "l1_bin32": dict(mode="binned", stage="l1", block=256, bin=32),
+    "l1_bin44": dict(mode="binned", stage="l1", block=256, bin=44),
+    "l1_bin60": dict(mode="binned", stage="l1", block=256, bin=60),
+    "l1_bin32_c16k": dict(mode="binned", stage="l1", block=256, bin=32, chunk=16384),
     "binned_l1_b128": dict(mode="binned", stage="l1", block=128, bin=8),
     "binned_tma": dict(mode="binned", block=256),
     "radix": dict(radix=1),
