@@ -329,6 +329,20 @@ def roofline(cfg_name, falg, n, eval_kernel_ms, step_ms, pk):
                              "peak": round(peak_gi, 1), "unit": "Gwarp-inst/s",
                              "frac": round(a / peak_gi, 4)}
         roof["profile"] = f"profiles/ncu_{cfg_name}.json ({d.get('source', '')})"
+    l2p = PROFILES / "r01_l2_bandwidth.json"
+    if l2p.exists():
+        # the coefficient gathers against the measured L2 read bandwidth (algorithmic bytes:
+        # one 4-B read per stencil site and coset)
+        from paper_2102_08518_b200 import load_fixture
+        c = CONFIGS[cfg_name]
+        sp = load_fixture(c["space"])
+        gbytes = 4 * sp.stencil_size * sp.ncosets
+        l2 = json.loads(l2p.read_text()).get("l2_gbs")
+        if l2:
+            a = gbytes * n / (eval_kernel_ms / 1e3) / 1e9
+            roof["l2_gathers"] = {"bytes_per_query": gbytes, "achieved": round(a, 1), "peak": l2,
+                                  "unit": "GB/s", "frac": round(a / l2, 4),
+                                  "peak_source": "profiles/r01_l2_bandwidth.json"}
     return roof
 
 
