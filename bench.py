@@ -59,6 +59,11 @@ CONFIGS = {
     "c4v": dict(space="fcc_voronoi2", extents=(161, 161, 161), queries=1 << 26, kind="uniform",
                 grad=True, scaling="weak", variant=dict(mode="direct", coeffs="table", block=128),
                 desc="FCC Voronoi spline (order 2), 4x161^3, 2^26 uniform, value + gradient"),
+    "c5u": dict(space="bcc_voronoi2", extents=(406, 406, 406), queries=1 << 30, kind="uniform",
+                grad=False, scaling="strong",
+                variant=dict(mode="binned", stage="l1", block=256, bin=136, coeffs="imm"),
+                desc="c5 with uniform random queries (SURVEY 8d secondary): 535 MB volume > L2; "
+                     "a coarse locality sort (136-cell bins, no bricks) keeps the gathers in L2"),
     "c3r": dict(space="bcc_voronoi2", extents=(203, 203, 203), queries=1 << 26, kind="render",
                 rays=(512, 512, 256), grad=False, scaling="weak", variant=dict(),
                 desc="fused volume render of c3: 512x512 rays x 256 samples through 2x203^3 BCC "

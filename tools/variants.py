@@ -63,6 +63,14 @@ VARIANTS = {
     "l1_bin44": dict(mode="binned", stage="l1", block=256, bin=44),
     "l1_bin60": dict(mode="binned", stage="l1", block=256, bin=60),
     "l1_bin32_c16k": dict(mode="binned", stage="l1", block=256, bin=32, chunk=16384),
+    "l1_bin84": dict(mode="binned", stage="l1", block=256, bin=84),
+    "l1_bin104": dict(mode="binned", stage="l1", block=256, bin=104),
+    "l1_bin136": dict(mode="binned", stage="l1", block=256, bin=136),
+    "l1_bin204": dict(mode="binned", stage="l1", block=256, bin=204),
+    "l1_bin104_b512": dict(mode="binned", stage="l1", block=512, bin=104),
+    "l1_bin60_b512": dict(mode="binned", stage="l1", block=512, bin=60),
+    "l1_bin60_b128": dict(mode="binned", stage="l1", block=128, bin=60),
+    "l1_bin60_c16k": dict(mode="binned", stage="l1", block=256, bin=60, chunk=16384),
     "binned_l1_b128": dict(mode="binned", stage="l1", block=128, bin=8),
     "binned_tma": dict(mode="binned", block=256),
     "radix": dict(radix=1),
