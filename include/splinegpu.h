@@ -28,7 +28,9 @@
  *
  * Ownership: the caller owns xs/out/grad/dbg (device pointers for sg_eval, host
  * pointers for sg_eval_host); the library owns modules and volumes.  All calls are
- * thread-safe per (module, stream); the only global mutable state is the
+ * thread-safe per (module, stream); a binned module owns one sort scratch, so its
+ * launches on different streams are ordered behind one another (an event per module)
+ * while the host path's copies still overlap.  The only global mutable state is the
  * thread-local error string.  Every entry point returns an SG_* status.
  */
 #ifndef SPLINEGPU_H

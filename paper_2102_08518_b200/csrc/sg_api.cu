@@ -89,6 +89,9 @@ struct sg_module {
   cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
   // binned mode: sorted queries + per-bin counts/starts/cursors (one stream at a time)
   std::mutex bin_mu;
+  // the binning scratch is one buffer per module: launches on different streams (the
+  // pipelined host path, or callers) are ordered behind the previous one with this event
+  cudaEvent_t bin_done = nullptr;
   void* bin_scratch = nullptr;
   size_t bin_scratch_bytes = 0;
   int64_t nbins = 0;
@@ -649,6 +652,7 @@ int sg_module_free(sg_module* m) {
     if (s) cudaStreamDestroy(s);
   if (m->scratch) cudaFree(m->scratch);
   if (m->bin_scratch) cudaFree(m->bin_scratch);
+  if (m->bin_done) cudaEventDestroy(m->bin_done);
   for (auto& pr : m->t_events) {
     cudaEventDestroy(pr.first);
     cudaEventDestroy(pr.second);
@@ -927,6 +931,8 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
   int* mat = (int*)((char*)m->bin_scratch + head);
   int2* items = (int2*)((char*)mat + (((size_t)mlen * sizeof(int) + 15) & ~(size_t)15));
   float4* sorted = (float4*)(((uintptr_t)(items + max_items) + 255) & ~(uintptr_t)255);
+  if (!m->bin_done) CU(cudaEventCreateWithFlags(&m->bin_done, cudaEventDisableTiming));
+  CU(cudaStreamWaitEvent(st, m->bin_done, 0));   // the previous launch has released the scratch
   BinGeom g{};
   g.dim = in.dim;
   g.bin = in.bin;
@@ -1013,8 +1019,11 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
   const void* itp = items;
   void* args[] = {(void*)&sp, (void*)&stp, (void*)&itp, (void*)&out, (void*)&grad, (void*)&dbg,
                   (void*)&err, (void*)&cs, (void*)&tm};
-  return timed_launch(m, (const void*)m->kernel, dim3((unsigned)max_items), dim3(in.block), args,
-                      (size_t)in.smem_bytes, st);
+  int rc = timed_launch(m, (const void*)m->kernel, dim3((unsigned)max_items), dim3(in.block), args,
+                        (size_t)in.smem_bytes, st);
+  if (rc) return rc;
+  CU(cudaEventRecord(m->bin_done, st));
+  return SG_OK;
   return SG_OK;
 }
 

@@ -196,3 +196,25 @@ def test_reference_contract_interpret_batch():
     got = interpret_batch(prog, xs, data)
     assert got.shape == (xs.shape[0],) and got.dtype == np.float64
     assert close(got, z["uniform_value"], RTOL_F32, ATOL_F32).all()
+
+
+def test_binned_module_on_two_streams():
+    """One binned module (one sort scratch) used from two streams at once: the library
+    orders the launches, so both results equal the single-stream ones."""
+    from paper_2102_08518_b200 import runtime
+    space, _, z, arrays = load_golden("bcc_box5")
+    ev = _evaluator(space, arrays, mode="binned")
+    rng = np.random.default_rng(5)
+    E = np.array(arrays[0].shape, np.float32)
+    xa = torch.from_numpy((rng.random((300000, 3)) * E).astype(np.float32)).cuda()
+    xb = torch.from_numpy((rng.random((200000, 3)) * E).astype(np.float32)).cuda()
+    want_a, want_b = ev(xa).clone(), ev(xb).clone()
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    oa = torch.empty(xa.shape[0], device="cuda")
+    ob = torch.empty(xb.shape[0], device="cuda")
+    torch.cuda.synchronize()
+    for _ in range(5):
+        runtime.eval_device(ev.module, ev.volume, xa, oa, stream=sa)
+        runtime.eval_device(ev.module, ev.volume, xb, ob, stream=sb)
+    torch.cuda.synchronize()
+    assert torch.equal(oa, want_a) and torch.equal(ob, want_b)
