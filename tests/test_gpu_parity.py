@@ -218,3 +218,20 @@ def test_binned_module_on_two_streams():
         runtime.eval_device(ev.module, ev.volume, xb, ob, stream=sb)
     torch.cuda.synchronize()
     assert torch.equal(oa, want_a) and torch.equal(ob, want_b)
+
+
+@pytest.mark.parametrize("mode", ["direct", "binned", "sorted"])
+def test_empty_and_tiny_batches(mode):
+    """n = 0 is a no-op; n = 1 and n = 33 (ragged tiles / warps) match the oracle."""
+    space, ospace, z, arrays = load_golden("bcc_voronoi2")
+    ev = _evaluator(space, arrays, mode=mode)
+    out = ev(torch.zeros((0, 3), dtype=torch.float32, device="cuda"))
+    assert out.shape == (0,)
+    for n in (1, 33):
+        xs = z["uniform_xs"][:n].astype(np.float32)
+        got = ev(torch.from_numpy(xs).cuda()).double().cpu().numpy()
+        want = refeval.reference_eval_batch(ospace, xs.astype(np.float64),
+                                            [a.astype(np.float64) for a in arrays])
+        assert close(got, want, RTOL_F32, ATOL_F32).all()
+    host = ev.eval_host(z["uniform_xs"][:0].astype(np.float32))
+    assert host.shape == (0,)
