@@ -381,7 +381,6 @@ __global__ void __launch_bounds__(SG_SORT_THREADS) sg_bin_scatter(
 
 // K3': tile-local counting sort before the scatter: records of one bin leave the CTA as
 // contiguous runs (coalesced 16-B stores) instead of one scattered store per query.
-constexpr int SG_TILE = 4096;   // records per tile of the 1024-thread instantiation
 constexpr int SG_TILED_MAX_BINS = 2048;   // per-tile histogram cost grows with the bin count
 
 template <int THREADS, int GROUPS>
