@@ -84,6 +84,10 @@ typedef struct sg_module_info {
   int64_t extents[SG_MAX_DIM]; /* unpadded extents (equal for all cosets in binned mode) */
   int32_t chunk;               /* binned: queries per CTA work item */
   int32_t static_smem;         /* informational: static shared memory of the kernel */
+  /* direct-mode kernels generated with presort: the library first counting-sorts the
+   * queries by cubes of `bin` cells (the binned-mode sort, for locality only) and the
+   * kernel reads the (x, y, z, original index) records, writing results by index */
+  int32_t presort;
 } sg_module_info;
 
 enum { SG_MODE_DIRECT = 0, SG_MODE_BINNED = 1, SG_MODE_RENDER = 2 };

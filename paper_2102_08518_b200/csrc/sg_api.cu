@@ -622,6 +622,18 @@ int sg_module_load(const void* image, size_t image_len, const char* entry, int d
       }
     }
   }
+  if (m->info.mode == SG_MODE_DIRECT && m->info.presort) {
+    if (m->info.dtype != SG_F32 || m->info.dim > 3 || m->info.bin < 1) {
+      cudaLibraryUnload(m->lib);
+      delete m;
+      return fail(SG_EINVAL, "presort needs f32 queries of dimension <= 3 and a bin >= 1");
+    }
+    m->nbins = 1;
+    for (int d = 0; d < m->info.dim; ++d) {
+      m->nb[d] = (m->info.extents[d] + m->info.bin - 1) / m->info.bin;
+      m->nbins *= m->nb[d];
+    }
+  }
   if ((m->info.mode == SG_MODE_DIRECT || m->info.mode == SG_MODE_RENDER) && m->info.smem_bytes > 0) {
     // sorted direct kernels keep their per-tile pair records in dynamic shared memory
     e = cudaFuncSetAttribute((const void*)m->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -633,8 +645,9 @@ int sg_module_load(const void* image, size_t image_len, const char* entry, int d
       return fail(SG_ECUDA, "smem attribute: %s", cudaGetErrorString(e));
     }
   }
-  e = cudaMalloc(&m->d_err, sizeof(unsigned));
-  if (e == cudaSuccess) e = cudaMemset(m->d_err, 0, sizeof(unsigned));
+  // err[0]: sticky error flags; err[1]: the sorted kernels' tile counter (zeroed per launch)
+  e = cudaMalloc(&m->d_err, 2 * sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMemset(m->d_err, 0, 2 * sizeof(unsigned));
   if (e != cudaSuccess) {
     cudaLibraryUnload(m->lib);
     delete m;
@@ -868,10 +881,13 @@ static int check_pair(const sg_module* m, const sg_volume* v) {
   return SG_OK;
 }
 
-static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64_t n, void* out,
-                         void* grad, int32_t* dbg, cudaStream_t st) {
+// Counting sort of the queries by coset-0 cell bins into the module's scratch (caller holds
+// bin_mu): sg_bin_count -> sg_bin_plan -> sg_bin_scatter_tiled.  Used by binned evaluation
+// (bricks per bin) and by presort kernels (locality only).  The launch is ordered behind the
+// module's previous one (bin_done); the caller records bin_done after its evaluation kernel.
+static int sort_queries(sg_module* m, const void* xs, int64_t n, cudaStream_t st, float4** sorted_out,
+                        int** starts_out, int2** items_out, long long* max_items_out) {
   const sg_module_info& in = m->info;
-  std::lock_guard<std::mutex> lock(m->bin_mu);
   const size_t nb = (size_t)m->nbins;
   if (nb > (size_t)SG_SMEM_BINS)
     return fail(SG_EINVAL, "%zu bins exceed the %d supported by the binning kernels; use a larger bin",
@@ -985,6 +1001,23 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
         (const float*)xs, (long long)n, per, g, mat, cursor, sorted);
   }
   CU(cudaGetLastError());
+  *sorted_out = sorted;
+  *starts_out = starts;
+  *items_out = items;
+  *max_items_out = max_items;
+  return SG_OK;
+}
+
+static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64_t n, void* out,
+                         void* grad, int32_t* dbg, cudaStream_t st) {
+  const sg_module_info& in = m->info;
+  std::lock_guard<std::mutex> lock(m->bin_mu);
+  float4* sorted = nullptr;
+  int* starts = nullptr;
+  int2* items = nullptr;
+  long long max_items = 0;
+  int rc0 = sort_queries(m, xs, n, st, &sorted, &starts, &items, &max_items);
+  if (rc0) return rc0;
   SgCosets cs{};
   for (int c = 0; c < v->ncosets; ++c) cs.base[c] = v->origin[c];
   static thread_local SgTmaps tm;
@@ -1030,6 +1063,18 @@ static int launch(sg_module* m, const sg_volume* v, const void* xs, int64_t n, v
                   void* grad, int32_t* dbg, cudaStream_t st) {
   if (n <= 0) return SG_OK;
   if (m->info.mode == SG_MODE_BINNED) return launch_binned(m, v, xs, n, out, grad, dbg, st);
+  std::unique_lock<std::mutex> presort_lock;
+  if (m->info.presort) {
+    // locality pre-sort: the kernel reads (x, y, z, index) records in bin order
+    presort_lock = std::unique_lock<std::mutex>(m->bin_mu);
+    float4* sorted = nullptr;
+    int* starts = nullptr;
+    int2* items = nullptr;
+    long long max_items = 0;
+    int rc0 = sort_queries(m, xs, n, st, &sorted, &starts, &items, &max_items);
+    if (rc0) return rc0;
+    xs = sorted;
+  }
   SgCosets cs{};
   for (int c = 0; c < v->ncosets; ++c) cs.base[c] = v->origin[c];
   long long nn = (long long)n;
@@ -1060,8 +1105,12 @@ static int launch(sg_module* m, const sg_volume* v, const void* xs, int64_t n, v
     cap = (long long)sms * occ;
   }
   grid = std::min(grid, cap);
-  return timed_launch(m, (const void*)m->kernel, dim3((unsigned)grid), dim3(m->info.block), args,
-                      (size_t)std::max(0, m->info.smem_bytes), st, v->alloc, v->bytes);
+  if (m->info.smem_bytes > 0 && m->info.mode == SG_MODE_DIRECT)
+    CU(cudaMemsetAsync(m->d_err + 1, 0, sizeof(unsigned), st));   // sorted kernels' tile counter
+  int rc = timed_launch(m, (const void*)m->kernel, dim3((unsigned)grid), dim3(m->info.block), args,
+                        (size_t)std::max(0, m->info.smem_bytes), st, v->alloc, v->bytes);
+  if (rc) return rc;
+  if (m->info.presort) CU(cudaEventRecord(m->bin_done, st));
   return SG_OK;
 }
 

@@ -72,6 +72,7 @@ class GenConfig:
     prefetch: int = 0            # sorted: load the next pair's record + coefficients one iteration ahead
     radix: int = 0               # 1: sub-region via a mixed-radix index of the plane-family counts
     rank: str = "match"          # sorted: rank in the psi class by "match" (warp-aggregated) | "atomic"
+    presort: int = 0             # sorted: bin edge (cells) of a locality pre-sort of the queries (0 = off)
 
     def __post_init__(self):
         if self.float_width not in (F64, F32):
@@ -450,6 +451,7 @@ class CudaProgram:
     smem_bytes: int = 0
     chunk: int = 0
     queries_per_thread: int = 1   # sorted mode: tile / block (one CTA tile per grid step)
+    presort: int = 0              # bin edge of the C ABI's locality pre-sort (sorted mode)
     stage_tma: bool = False
     rounding: int = 1
     meta: dict = field(default_factory=dict)
@@ -552,6 +554,11 @@ def generate(space, config: GenConfig | None = None, extents=None,
     # RB rays x (tile / RB) steps are sorted by psi like queries of a sorted tile)
     sorted_ = cfg.mode == "sorted" or (render and cfg.tile > 0)
     RB = 128   # sorted render: rays per CTA block (four 8 x 4-pixel warp tiles)
+    presort = cfg.presort if (sorted_ and not render) else 0
+    if cfg.presort and not presort:
+        raise ValueError("presort applies to mode='sorted' (query kernels)")
+    if presort and (s > 3 or len(set(ext)) != 1):
+        raise ValueError("presort needs equal coset extents and dimension <= 3")
     pack2 = cfg.pack == 2
     if pack2:
         if cfg.float_width != F32 or cfg.mode not in ("direct", "binned"):
@@ -925,7 +932,10 @@ def generate(space, config: GenConfig | None = None, extents=None,
             for l in range(M):
                 B(f"  const int coff{l} = (int)((const float*)vol.base[{l}] - (const float*)vol.base[0]);")
             B("  __syncthreads();")
-            sorted_smem = MP * pair_bytes
+            sorted_smem = MP * pair_bytes + (TQ * 4 if presort else 0)
+            if presort:
+                # original index of every tile query (the input is the locality-sorted records)
+                B(f"  int* sg_qidx = reinterpret_cast<int*>(sg_dyn + {MP * pair_bytes});")
             ind = "  "
             if render:
                 B(f"  const float tf_lo = tf[0], tf_inv = tf[1], tf_op = tf[2];")
@@ -943,7 +953,15 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 B(f"  for (int j0 = 0; j0 < steps; j0 += {TQ // RB}) {{")
             else:
                 # persistent tiles: the shared tables are staged once per CTA
-                B(f"  for (long long q0 = (long long)blockIdx.x * {TQ}; q0 < n; q0 += (long long)gridDim.x * {TQ}) {{")
+                # tiles are claimed in order from a per-launch counter (err[1], zeroed by the
+                # C ABI before the launch): the resident CTAs work on a contiguous window of
+                # the query stream -- coherent L1/L2 footprint, no tail imbalance
+                B("  __shared__ long long sg_q0;")
+                B("  for (;;) {")
+                B(f"  if (threadIdx.x == 0) sg_q0 = (long long)atomicAdd(err + 1, 1u) * {TQ};")
+                B("  __syncthreads();")
+                B("  const long long q0 = sg_q0;")
+                B("  if (q0 >= n) break;")
         elif smem:
             B("  __syncthreads();")
         if sorted_:
@@ -1918,11 +1936,22 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 for d, (oc, dc) in enumerate((("ra.x", "ra.w"), ("ra.y", "rb.x"), ("ra.z", "rb.y"))):
                     body.append(f"    const float xq{d} = __fadd_rn({oc}, __fmul_rn(tj, {dc}));")
                     body.append(f"    const double x{d} = (double)xq{d};")
+            elif presort:
+                # records (x, y, z, original index) in locality order: the tile's queries are
+                # spatially close, so the coefficient gathers stay in L1/L2
+                body.append("    const long long qs_ = q0 + ql;")
+                body.append("    const bool valid = qs_ < n;")
+                body.append(f"    const float4 r4_ = {ldf}(reinterpret_cast<const float4*>(xs) + (valid ? qs_ : n - 1));")
+                body.append("    const long long qi = (long long)__float_as_int(r4_.w);")
+                body.append("    if (valid) sg_qidx[ql] = (int)qi;")
+                for d in range(s):
+                    body.append(f"    const float xq{d} = r4_.{'xyz'[d]};")
+                    body.append(f"    const double x{d} = (double)xq{d};")
             else:
                 body.append("    const long long qi = q0 + ql;")
                 body.append("    const bool valid = qi < n;")
                 body.append("    const long long qc = valid ? qi : n - 1;")
-            for d in range(s if not render else 0):
+            for d in range(s if not (render or presort) else 0):
                 if intsel:
                     body.append(f"    const float xq{d} = {ldf}(&xs[qc * {s} + {d}]);")
                     body.append(f"    const double x{d} = (double)xq{d};")
@@ -2068,8 +2097,12 @@ def generate(space, config: GenConfig | None = None, extents=None,
     if sorted_ and not render:
         # phase 3: coset contributions summed in coset order, coalesced stores
         body.append(f"    for (int ql = threadIdx.x; ql < {TQ}; ql += {Bk}) {{")
-        body.append("      const long long qi = q0 + ql;")
-        body.append("      if (qi >= n) break;")
+        if presort:
+            body.append("      if (q0 + ql >= n) break;")
+            body.append("      const long long qi = (long long)sg_qidx[ql];")
+        else:
+            body.append("      const long long qi = q0 + ql;")
+            body.append("      if (qi >= n) break;")
         if cfg.grad:
             body.append("      float4 a_ = sg_res4[ql];")
             for l in range(1, M):
@@ -2151,6 +2184,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
         stage_tma=binned and cfg.stage == "tma",
         chunk=cfg.chunk if binned else 0,
         queries_per_thread=cfg.tile // cfg.block if sorted_ else 1,
+        presort=presort,
         rounding=(0 if (rm0.shape == PARALLELEPIPED and rm0.rounding == "floor") else 1),
         meta={"fetch_mode": fetch_mode, "K": t.K, "nsub": t.nsub, "n": t.n, "reach": h,
               "smem_tables": [x[0] for x in smem], "lut_entries": len(lut)})

@@ -48,7 +48,7 @@ class sg_module_info(ctypes.Structure):
                 ("stage_tma", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
                 ("bin", ctypes.c_int32), ("brick", ctypes.c_int32 * SG_MAX_DIM),
                 ("extents", ctypes.c_int64 * SG_MAX_DIM), ("chunk", ctypes.c_int32),
-                ("static_smem", ctypes.c_int32)]
+                ("static_smem", ctypes.c_int32), ("presort", ctypes.c_int32)]
 
 
 _lib = None
@@ -197,6 +197,10 @@ class Module:
             info.brick[d] = e
         for d, e in enumerate(prog.extents[0]):
             info.extents[d] = e
+        if getattr(prog, "presort", 0):
+            info.presort = 1
+            info.bin = prog.presort
+            info.chunk = 1 << 16        # the sort's work-item list is unused here: keep it short
         h = ctypes.c_void_p()
         buf = ctypes.create_string_buffer(self.image, len(self.image))
         _check(lib().sg_module_load(buf, len(self.image), prog.entry.encode(), device,

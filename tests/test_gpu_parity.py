@@ -38,11 +38,13 @@ def _xs(z, which, dtype=torch.float32):
 
 @pytest.mark.parametrize("name", golden_names())
 @pytest.mark.parametrize("mode", ["direct", "binned", "sorted", "direct_f64", "pack2", "pack2_binned",
-                                  "radix", "radix_f64"])
+                                  "radix", "radix_f64", "presort"])
 def test_selection_bit_exact(name, mode):
     space, _, z, arrays = load_golden(name)
     if mode == "direct_f64":
         ev = _evaluator(space, arrays, dbg=True, select="f64")
+    elif mode == "presort":
+        ev = _evaluator(space, arrays, dbg=True, mode="sorted", presort=4)
     elif mode.startswith("radix"):
         ev = _evaluator(space, arrays, dbg=True, radix=1, mode="sorted",
                         select="f64" if mode.endswith("f64") else "auto")
@@ -84,6 +86,8 @@ CONFIGS = [
     dict(radix=1),
     dict(radix=1, mode="sorted", select="f64"),
     dict(mode="sorted", rank="atomic", radix=1),
+    dict(mode="sorted", presort=4, radix=1),
+    dict(mode="sorted", presort=8, form="sym", tile=512, block=256),
     dict(pack=2, mode="binned", form="sym"),
     dict(pack=2, form="sites", params_md=(2, 4)),
     dict(pack=2, mode="binned", block=256, select="f64"),
@@ -133,7 +137,7 @@ def test_values_f64_variant(name):
 
 @pytest.mark.parametrize("name", golden_names())
 @pytest.mark.parametrize("mode", ["direct", "binned", "table", "sym", "sorted", "sorted_sym",
-                                  "pack2", "pack2_binned_sym"])
+                                  "pack2", "pack2_binned_sym", "presort"])
 def test_gradient_vs_oracle(name, mode):
     space, ospace, z, arrays = load_golden(name)
     xs = z["uniform_xs"].astype(np.float64)
@@ -147,6 +151,8 @@ def test_gradient_vs_oracle(name, mode):
         ev = _evaluator(space, arrays, grad=True, form="sym", mode="sorted", block=256)
     elif mode == "pack2":
         ev = _evaluator(space, arrays, grad=True, pack=2)
+    elif mode == "presort":
+        ev = _evaluator(space, arrays, grad=True, mode="sorted", presort=4)
     elif mode == "pack2_binned_sym":
         ev = _evaluator(space, arrays, grad=True, pack=2, mode="binned", form="sym")
     else:
@@ -158,10 +164,15 @@ def test_gradient_vs_oracle(name, mode):
 
 
 @pytest.mark.parametrize("name", golden_names())
-@pytest.mark.parametrize("mode", ["direct", "binned", "sorted", "pack2"])
+@pytest.mark.parametrize("mode", ["direct", "binned", "sorted", "pack2", "presort"])
 def test_host_path_matches_device_path(name, mode):
     space, _, z, arrays = load_golden(name)
-    ev = _evaluator(space, arrays, pack=2) if mode == "pack2" else _evaluator(space, arrays, mode=mode)
+    if mode == "pack2":
+        ev = _evaluator(space, arrays, pack=2)
+    elif mode == "presort":
+        ev = _evaluator(space, arrays, mode="sorted", presort=4)
+    else:
+        ev = _evaluator(space, arrays, mode=mode)
     xs = z["uniform_xs"]
     dev = ev(torch.from_numpy(xs).cuda()).cpu().numpy()
     host = ev.eval_host(xs, chunk=257)

@@ -73,6 +73,9 @@ VARIANTS = {
     "l1_bin60_c16k": dict(mode="binned", stage="l1", block=256, bin=60, chunk=16384),
     "binned_l1_b128": dict(mode="binned", stage="l1", block=128, bin=8),
     "binned_tma": dict(mode="binned", block=256),
+    "presort136": dict(mode="sorted", block=512, radix=1, presort=136),
+    "presort104": dict(mode="sorted", block=512, radix=1, presort=104),
+    "presort68": dict(mode="sorted", block=512, radix=1, presort=68),
     "radix": dict(radix=1),
     "rank_atomic": dict(rank="atomic"),
     "radix_direct": dict(radix=1, mode="direct", block=128),
