@@ -1145,6 +1145,7 @@ int sg_render(sg_module* m, const sg_volume* v, const float* rays, int64_t npix,
         occ < 1)
       occ = 1;
     grid = std::min((nn + 127) / 128, (long long)sms * occ);
+    CU(cudaMemsetAsync(m->d_err + 1, 0, sizeof(unsigned), (cudaStream_t)stream));   // block counter
   }
   return timed_launch(m, (const void*)m->kernel, dim3((unsigned)grid), dim3(m->info.block), args,
                       (size_t)std::max(0, m->info.smem_bytes), (cudaStream_t)stream, v->alloc,

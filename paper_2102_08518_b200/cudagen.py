@@ -944,7 +944,12 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 if cfg.grad:
                     B("  const float L0 = tf[9], L1 = tf[10], L2 = tf[11];")
                 # persistent ray blocks; each block marches its RB rays in chunks of SJ steps
-                B(f"  for (long long rb0 = (long long)blockIdx.x * {RB}; rb0 < n; rb0 += (long long)gridDim.x * {RB}) {{")
+                B("  __shared__ long long sg_rb0;")
+                B("  for (;;) {   // ray blocks claimed in order from the per-launch counter err[1]")
+                B(f"  if (threadIdx.x == 0) sg_rb0 = (long long)atomicAdd(err + 1, 1u) * {RB};")
+                B("  __syncthreads();")
+                B("  const long long rb0 = sg_rb0;")
+                B("  if (rb0 >= n) break;")
                 B(f"  const long long myray = rb0 + threadIdx.x;")
                 B(f"  float my_dt = 0.f;")
                 B(f"  if (threadIdx.x < {RB} && myray < n) my_dt = __ldg(&rays[2 * myray + 1]).w;")
@@ -2092,6 +2097,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
             body.append("    __syncthreads();")
             body.append("  }")   # step chunks
             body.append(f"  if (threadIdx.x < {RB} && myray < n) {stf}(&rgba[myray], make_float4(C0, C1, C2, A));")
+            body.append("  __syncthreads();   // sg_rb0 is rewritten by the next claim")
             body.append("  }")   # ray blocks
             body.append("}")
     if sorted_ and not render:
