@@ -7,6 +7,7 @@ path through the C ABI (GPU) or on generated sources (CPU):
   branchy == predicated (K = 2)                            :238-244
   fetch count == n * M                                     :395-402
   shift invariance (integer steps, coset permutation)      tests/test_oracle.py:108-129
+  triple agreement (kernel / evaluator / convolution)      tests/test_acceptance.py:38-83
 """
 
 from fractions import Fraction as F
@@ -122,3 +123,20 @@ def test_shift_invariance_permutes_cosets():
     shifted = [np.roll(arrays[1], 1), arrays[0]]
     got = _values("halfgrid1d", pts + np.float32(0.5), arrays=shifted)
     assert np.abs(got - base).max() <= 1e-5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["zp", "trilinear_voronoi", "halfgrid1d", "bcc_box_linear"])
+def test_triple_agreement_cuda_oracle_convolution(name):
+    """Reference tests/test_acceptance.py:38-83: the generated program, the reference
+    evaluator and the direct convolution sum agree -- here the CUDA kernel takes the
+    generated program's place."""
+    from oracle import refeval
+    space, ospace, z, arrays = load_golden(name)
+    xs = z["uniform_xs"][:400].astype(np.float32)
+    a64 = [a.astype(np.float64) for a in arrays]
+    cuda = _values(name, xs)
+    ref = refeval.reference_eval_batch(ospace, xs.astype(np.float64), a64)
+    conv = refeval.convolution_eval_batch(ospace, xs.astype(np.float64), a64)
+    assert np.abs(ref - conv).max() <= 1e-9
+    assert np.all(np.abs(cuda - ref) <= 1e-6 + 1e-5 * np.maximum(np.abs(cuda), np.abs(ref)))

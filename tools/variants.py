@@ -73,6 +73,11 @@ VARIANTS = {
     "l1_bin60_c16k": dict(mode="binned", stage="l1", block=256, bin=60, chunk=16384),
     "binned_l1_b128": dict(mode="binned", stage="l1", block=128, bin=8),
     "binned_tma": dict(mode="binned", block=256),
+    "srt_b256_t1024": dict(mode="sorted", block=256, tile=1024, radix=1),
+    "srt_b256_t768": dict(mode="sorted", block=256, tile=768, radix=1),
+    "srt_b384_t1152": dict(mode="sorted", block=384, tile=1152, radix=1),
+    "srt_b512_t1024": dict(mode="sorted", block=512, tile=1024, radix=1),
+    "srt_b640_t1280": dict(mode="sorted", block=640, tile=1280, radix=1),
     "presort136": dict(mode="sorted", block=512, radix=1, presort=136),
     "presort104": dict(mode="sorted", block=512, radix=1, presort=104),
     "presort68": dict(mode="sorted", block=512, radix=1, presort=68),
