@@ -140,3 +140,21 @@ def test_triple_agreement_cuda_oracle_convolution(name):
     conv = refeval.convolution_eval_batch(ospace, xs.astype(np.float64), a64)
     assert np.abs(ref - conv).max() <= 1e-9
     assert np.all(np.abs(cuda - ref) <= 1e-6 + 1e-5 * np.maximum(np.abs(cuda), np.abs(ref)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["zp", "zp_k2", "trilinear", "trilinear_voronoi", "halfgrid1d",
+                                  "linear1d", "tricubic", "bcc_box5", "bcc_box_linear",
+                                  "bcc_voronoi2", "fcc_box6", "fcc_voronoi2"])
+def test_partition_of_unity_every_space(name):
+    """Reference tests/test_acceptance.py:86-93: all-ones data reconstruct 1 everywhere
+    (per coset the normalization of the spline, times the coset count for split lattices)."""
+    from oracle import refeval
+    space, ospace, z, arrays = load_golden(name)
+    ones = [np.ones_like(a, dtype=np.float32) for a in arrays]
+    xs = z["uniform_xs"].astype(np.float32)
+    got = _values(name, xs, arrays=ones)
+    want = refeval.reference_eval_batch(ospace, xs.astype(np.float64),
+                                        [a.astype(np.float64) for a in ones])
+    assert np.abs(want - want[0]).max() <= 1e-9          # constant, as the reference asserts
+    assert np.abs(got - want).max() <= 2e-6
