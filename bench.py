@@ -442,9 +442,10 @@ def run_ours(args, rank, world, device):
     e2e_steps = max(3, min(args.steps, 20))
     lib = runtime.lib()
 
-    # 2^22-query chunks: H2D, kernel and D2H overlap on 3 streams for the large configs;
-    # smaller chunks cost more in per-call fixed work (measured: c1 2^18 chunks 1.3 vs 1.8)
-    host_chunk = 1 << 22
+    # 2^21-query chunks (the library default): H2D, kernel and D2H overlap on 3 streams;
+    # measured on B200 (tools/e2e_chunks.py): c2 4.11 G/s at 2^21 vs 3.92 at 2^22 and 3.04 at
+    # 2^24; much smaller chunks lose to per-call fixed work (c1 at 2^18: 1.3 vs 1.8)
+    host_chunk = 1 << 21
 
     def host_step():
         runtime._check(lib.sg_eval_host(ev.module.handle, ev.volume.handle,
