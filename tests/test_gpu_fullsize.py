@@ -17,7 +17,7 @@ from paper_2102_08518_b200.model import SPACES_DIR  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
-CFGS = ["c1", "c2", "c3", "c4", "c4v"]
+CFGS = ["c1", "c2", "c3", "c4", "c4v", "c5", "c5u"]
 NQ = 1 << 20
 
 
