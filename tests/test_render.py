@@ -68,3 +68,25 @@ def test_render_rejects_eval_and_vice_versa():
     out = torch.empty(4, device="cuda")
     with pytest.raises(runtime.SplineGpuError):
         runtime.eval_device(r.ev.module, r.ev.volume, xs, out)
+
+
+@pytest.mark.gpu
+def test_render_full_size_constant_volume_closed_form():
+    """Bench-size render (512 x 512 x 256, the sorted tiles) of an all-ones volume: f = 1 at
+    every sample (partition of unity), so each ray composites a constant opacity
+    a = min(opacity * dt, 1): A = 1 - (1 - a)^steps, rgb = rgb_hi * A."""
+    from paper_2102_08518_b200 import load_fixture
+    from paper_2102_08518_b200.render import DEFAULT_TF, Renderer
+    space = load_fixture("bcc_voronoi2")
+    E = (203, 203, 203)
+    ones = [np.ones(E, dtype=np.float32) for _ in range(space.ncosets)]
+    r = Renderer(space, ones, 512, 512, 256)
+    img = r().cpu().numpy().reshape(-1, 4)
+    px, py = pixel_of(np.arange(512 * 512), 512)
+    dt = np.zeros((512, 512))
+    dt[py, px] = r.rays_np[:, 7]
+    a = np.minimum(DEFAULT_TF["opacity"] * dt.astype(np.float64), 1.0).reshape(-1)
+    A = 1.0 - (1.0 - a) ** 256
+    assert np.abs(img[:, 3] - A).max() <= 2e-4
+    for ch in range(3):
+        assert np.abs(img[:, ch] - DEFAULT_TF["rgb_hi"][ch] * A).max() <= 2e-4
