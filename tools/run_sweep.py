@@ -13,6 +13,7 @@ from paper_2102_08518_b200 import load_fixture, make_volume  # noqa: E402
 from paper_2102_08518_b200.sweep import emit_csv, emit_matrix, run_sweep  # noqa: E402
 
 EXTENTS = {"bcc_voronoi2": (101, 101, 101), "fcc_box6": (81, 81, 81), "zp_k2": (256, 256),
+           "bcc_box5": (101, 101, 101),
            "trilinear_voronoi": (64, 64, 64), "bcc_box_linear": (101, 101, 101)}
 
 
