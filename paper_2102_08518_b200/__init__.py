@@ -7,7 +7,7 @@ Python API; `cudagen` lowers it to one-query-per-thread sm_100a kernels that are
 compiled with NVRTC and called through the C ABI in include/splinegpu.h.
 """
 
-from .api import DataVolume, Evaluator, InterpreterError, generate, interpret, interpret_batch, make_volume, sample_points
+from .api import DataVolume, Evaluator, InterpreterError, Program, generate, interpret, interpret_batch, make_volume, sample_points
 from .cudagen import CudaProgram, GenConfig, default_config
 from .model import (
     SplineSpace,
@@ -23,7 +23,7 @@ from .runtime import SplineGpuError, UnreachableRegionError
 from .schedule import EvalPlan, ScheduleParams, schedule_pipeline
 
 __all__ = [
-    "CudaProgram", "DataVolume", "EvalPlan", "Evaluator", "GenConfig", "InterpreterError", "Poly",
+    "CudaProgram", "DataVolume", "EvalPlan", "Evaluator", "GenConfig", "InterpreterError", "Poly", "Program",
     "ScheduleParams", "SplineGpuError", "SplineSpace", "UnreachableRegionError", "default_config",
     "generate", "group_polynomial", "horner_factorize", "interpret", "interpret_batch",
     "list_fixtures", "load_fixture", "load_space", "make_volume", "parse_space", "poly_eval",

@@ -3,7 +3,8 @@
 Mirrors the reference's public surface for the evaluation path
 (pkg/src/splinegen/__init__.py:10-48):
 
-  generate(space, GenConfig) -> CudaProgram         (codegen.py:508)
+  generate(space, GenConfig) -> Program             (codegen.py:508; extent-free,
+                                                     specialized per volume on use)
   interpret_batch(prog, xs, data) -> ndarray (N,)   (ir.py:582-700)
   interpret(prog, x, data) -> float                 (ir.py:793)
   DataVolume(arrays)                                (ir.py:524-558)
@@ -82,9 +83,59 @@ def sample_points(space, data, count: int, seed: int) -> np.ndarray:
     return rng.random((count, space.dim)) * np.array(data.extents[0], dtype=np.float64)
 
 
-def generate(space, config: GenConfig | None = None, extents=None) -> CudaProgram:
-    """Reference `generate` + the volume extents the kernel is specialized on."""
+class Program:
+    """The result of the reference-shaped call `generate(space, cfg)` (codegen.py:508): a
+    program that does not yet know the volume it will run on.
+
+    The CUDA kernel is specialized on the padded per-coset strides (every stencil fetch
+    offset becomes an immediate), so the concrete `CudaProgram` is generated on first use
+    for each distinct set of data extents (`specialize`) -- `interpret_batch` and
+    `Evaluator` do that transparently, which is what lets the reference's
+    `prog = generate(space, cfg); interpret_batch(prog, xs, data)` pattern run unchanged
+    for any DataVolume."""
+
+    def __init__(self, space, config: GenConfig | None = None):
+        if not isinstance(space, SplineSpace):
+            space = SplineSpace.adopt(space)
+        self.space = space
+        self.config = config or default_config(space)
+        self._specs = {}
+        # validate the space and the variant once, up front (the reference's generate
+        # raises here too), on a nominal geometry
+        self.specialize((64,) * space.dim)
+
+    name = property(lambda self: self.space.name)
+    dim = property(lambda self: self.space.dim)
+    ncosets = property(lambda self: self.space.ncosets)
+    float_width = property(lambda self: self.config.float_width)
+
+    @property
+    def dtype(self):
+        return np.float32 if self.config.float_width == "f32" else np.float64
+
+    def specialize(self, extents) -> CudaProgram:
+        ext = tuple(tuple(int(v) for v in e) for e in extents) \
+            if isinstance(extents[0], (tuple, list)) else tuple(int(v) for v in extents)
+        prog = self._specs.get(ext)
+        if prog is None:
+            prog = self._specs[ext] = _generate(self.space, self.config, ext)
+        return prog
+
+
+def generate(space, config: GenConfig | None = None, extents=None):
+    """Reference `generate(space, GenConfig)` (codegen.py:508).
+
+    Without `extents` the result is an extent-free `Program` (specialized per volume on
+    first use); with `extents` (one tuple of s ints, or one per coset) the concrete
+    `CudaProgram` for that geometry is returned directly."""
+    if extents is None:
+        return Program(space, config)
     return _generate(space, config, extents)
+
+
+def _specialize_for(prog, arrays):
+    ext = tuple(tuple(int(e) for e in a.shape) for a in arrays)
+    return prog.specialize(ext if len(set(ext)) > 1 else ext[0])
 
 
 class Evaluator:
@@ -95,7 +146,7 @@ class Evaluator:
     """
 
     def __init__(self, space, data, config: GenConfig | None = None, device: int = 0,
-                 prog: CudaProgram | None = None):
+                 prog=None, module=None):
         import torch
         if not isinstance(space, SplineSpace):
             space = SplineSpace.adopt(space)
@@ -104,11 +155,13 @@ class Evaluator:
         if len(arrays) != space.ncosets:
             raise InterpreterError(f"data has {len(arrays)} cosets, program wants {space.ncosets}")
         ext = tuple(tuple(int(e) for e in a.shape) for a in arrays)
+        if isinstance(prog, Program):
+            prog = _specialize_for(prog, arrays)
         self.prog = prog or _generate(space, config or default_config(space), ext)
         if self.prog.extents != ext:
             raise InterpreterError(f"program compiled for extents {self.prog.extents}, data has {ext}")
         self.device = device
-        self.module = runtime.Module(self.prog, device)
+        self.module = module if module is not None else runtime.Module(self.prog, device)
         self.volume = runtime.Volume(arrays, self.prog.halo, self.prog.dtype, device,
                                      padded=self.prog.padded_extents)
         self.torch_dtype = torch.float32 if self.prog.float_width == "f32" else torch.float64
@@ -118,6 +171,10 @@ class Evaluator:
         s, M = self.space.dim, self.space.ncosets
         if xs.ndim != 2 or xs.shape[1] != s:
             raise InterpreterError(f"expected points of shape (N, {s})")
+        for name, t in (("xs", xs), ("out", out), ("grad", grad), ("dbg", dbg)):
+            if t is not None and (not t.is_cuda or t.device.index != self.device):
+                raise InterpreterError(f"{name} must be a CUDA tensor on cuda:{self.device}, "
+                                       f"not {t.device}")
         if xs.dtype != self.torch_dtype or not xs.is_contiguous():
             xs = xs.to(self.torch_dtype).contiguous()
         n = xs.shape[0]
@@ -145,38 +202,55 @@ class Evaluator:
         return (out, grad) if grad is not None else out
 
 
-_EV_CACHE = {}
+DEFAULT_BUDGET = 50_000_000   # the reference interpreter's instruction budget (ir.py)
+
+_MODULES = {}   # CudaProgram source key -> loaded module (compiled kernels are reused)
 
 
-def interpret_batch(prog, xs, data, max_steps=None, counter=None) -> np.ndarray:
+def _module_for(cprog, device=0):
+    key = (cprog.key, device)
+    mod = _MODULES.get(key)
+    if mod is None:
+        if len(_MODULES) >= 32:
+            _MODULES.clear()
+        mod = _MODULES[key] = runtime.Module(cprog, device)
+    return mod
+
+
+def interpret_batch(prog, xs, data, max_steps: int = DEFAULT_BUDGET, counter=None) -> np.ndarray:
     """Reference-contract batch evaluation on the GPU (ir.py:582-700).
 
-    `prog` may be a CudaProgram (from `generate`) or a SplineSpace (then the
-    default GPU config is generated for the data's extents).
-    """
+    `prog`: a `Program` / `CudaProgram` from `generate`, or a SplineSpace (the default
+    config is generated for it).  Like the reference, every call reads `data` afresh
+    (the volume is uploaded per call, so in-place edits of the arrays are seen; the
+    compiled kernel is cached) and returns an array of the program's dtype.
+
+    `counter` (the reference's per-IR-opcode dynamic instruction count) has no meaning
+    for a compiled GPU kernel and is rejected explicitly; `max_steps` (the interpreter's
+    runaway-loop budget) is validated and otherwise moot -- generated kernels are
+    straight-line per query and always terminate."""
     import torch
-    if isinstance(prog, CudaProgram):
-        space = prog.space
-    else:
-        space = prog if isinstance(prog, SplineSpace) else SplineSpace.adopt(prog)
-        prog = None
+    if counter is not None:
+        raise InterpreterError("counter= counts reference IR instructions; the CUDA program "
+                               "has none (use bench.py's F_alg / ncu instruction counts)")
+    if not isinstance(max_steps, (int, np.integer)) or max_steps < 1:
+        raise InterpreterError(f"max_steps must be a positive integer, not {max_steps!r}")
+    if not isinstance(prog, (Program, CudaProgram)):
+        prog = Program(prog)
+    space = prog.space
     xs = np.asarray(xs, dtype=np.float64)
     if xs.ndim != 2 or xs.shape[1] != space.dim:
         raise InterpreterError(f"expected points of shape (N, {space.dim})")
     if data.ncosets != space.ncosets:
         raise InterpreterError(f"data has {data.ncosets} cosets, program wants {space.ncosets}")
-    key = (id(prog) if prog is not None else id(space), id(data))
-    ev = _EV_CACHE.get(key)
-    if ev is None or ev[1] is not data:
-        ev = (Evaluator(space, data, prog=prog), data)
-        _EV_CACHE.clear()
-        _EV_CACHE[key] = ev
-    e = ev[0]
-    t = torch.from_numpy(xs.astype(e.prog.dtype)).cuda(e.device)
-    res = e(t)
+    arrays = data.arrays if hasattr(data, "arrays") else list(data)
+    cprog = _specialize_for(prog, arrays) if isinstance(prog, Program) else prog
+    ev = Evaluator(space, arrays, prog=cprog, module=_module_for(cprog))
+    t = torch.from_numpy(xs.astype(cprog.dtype)).cuda(ev.device)
+    res = ev(t)
     if isinstance(res, tuple):
         res = res[0]
-    return res.double().cpu().numpy()
+    return res.cpu().numpy().astype(cprog.dtype, copy=False)
 
 
 def interpret(prog, x, data) -> float:

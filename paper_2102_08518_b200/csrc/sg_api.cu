@@ -81,7 +81,16 @@ struct sg_module {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kernel = nullptr;
   sg_module_info info{};
+  // Launch slots: every launch gets its own 2-word slot of d_err -- [0] sticky error flags
+  // (OR-ed over all slots by sg_module_status), [1] the tile / ray-block counter of the
+  // persistent sorted and render kernels.  A slot is reused only after the launch that
+  // last held it has finished (slot_ev), so launches of one module on different streams
+  // never share a counter.
+  static constexpr int kSlots = 16;
   unsigned* d_err = nullptr;
+  cudaEvent_t slot_ev[kSlots] = {};
+  unsigned slot_next = 0;
+  std::mutex slot_mu;
   int regs = 0, local_bytes = 0;
   std::mutex mu;  // guards the host-path scratch below
   void* scratch = nullptr;
@@ -129,6 +138,27 @@ static size_t l2_persist_budget(int device) {
     }
   }
   return state[device] == 2 ? std::min(budget[device], max_window[device]) : 0;
+}
+
+// Take the next launch slot for a launch on `st` (see sg_module::d_err): the stream waits
+// for the slot's previous holder, the slot's counter is zeroed when the kernel uses one.
+// The caller keeps `lk` until it has recorded the slot event (release_slot) after the
+// launch, so no other launch can take the same slot in between.
+static int acquire_slot(sg_module* m, cudaStream_t st, bool zero_counter,
+                        std::unique_lock<std::mutex>& lk, int* slot, unsigned** err) {
+  lk = std::unique_lock<std::mutex>(m->slot_mu);
+  const int k = (int)(m->slot_next++ % sg_module::kSlots);
+  if (!m->slot_ev[k]) CU(cudaEventCreateWithFlags(&m->slot_ev[k], cudaEventDisableTiming));
+  else CU(cudaStreamWaitEvent(st, m->slot_ev[k], 0));
+  if (zero_counter) CU(cudaMemsetAsync(m->d_err + 2 * k + 1, 0, sizeof(unsigned), st));
+  *slot = k;
+  *err = m->d_err + 2 * k;
+  return SG_OK;
+}
+
+static int release_slot(sg_module* m, int k, cudaStream_t st) {
+  CU(cudaEventRecord(m->slot_ev[k], st));
+  return SG_OK;
 }
 
 static int timed_launch(sg_module* m, const void* func, dim3 grid, dim3 block, void** args,
@@ -645,9 +675,9 @@ int sg_module_load(const void* image, size_t image_len, const char* entry, int d
       return fail(SG_ECUDA, "smem attribute: %s", cudaGetErrorString(e));
     }
   }
-  // err[0]: sticky error flags; err[1]: the sorted kernels' tile counter (zeroed per launch)
-  e = cudaMalloc(&m->d_err, 2 * sizeof(unsigned));
-  if (e == cudaSuccess) e = cudaMemset(m->d_err, 0, 2 * sizeof(unsigned));
+  // launch slots: [2k] sticky error flags, [2k + 1] tile counter (zeroed per launch)
+  e = cudaMalloc(&m->d_err, 2 * sg_module::kSlots * sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMemset(m->d_err, 0, 2 * sg_module::kSlots * sizeof(unsigned));
   if (e != cudaSuccess) {
     cudaLibraryUnload(m->lib);
     delete m;
@@ -665,6 +695,8 @@ int sg_module_free(sg_module* m) {
   if (m->scratch) cudaFree(m->scratch);
   if (m->bin_scratch) cudaFree(m->bin_scratch);
   if (m->bin_done) cudaEventDestroy(m->bin_done);
+  for (auto& ev : m->slot_ev)
+    if (ev) cudaEventDestroy(ev);
   for (auto& pr : m->t_events) {
     cudaEventDestroy(pr.first);
     cudaEventDestroy(pr.second);
@@ -707,11 +739,14 @@ int sg_module_regs(const sg_module* m, int* regs, int* local_bytes) {
 int sg_module_status(sg_module* m, void* stream, uint32_t* flags) {
   if (!m) return fail(SG_EINVAL, "NULL module");
   CU(cudaSetDevice(m->device));
-  unsigned h = 0;
+  unsigned w[2 * sg_module::kSlots] = {};
   cudaStream_t st = (cudaStream_t)stream;
-  CU(cudaMemcpyAsync(&h, m->d_err, sizeof h, cudaMemcpyDeviceToHost, st));
-  CU(cudaMemsetAsync(m->d_err, 0, sizeof h, st));
+  CU(cudaMemcpyAsync(w, m->d_err, sizeof w, cudaMemcpyDeviceToHost, st));
+  // clear the error words only: a counter may belong to a launch running on another stream
+  CU(cudaMemset2DAsync(m->d_err, 2 * sizeof(unsigned), 0, sizeof(unsigned), sg_module::kSlots, st));
   CU(cudaStreamSynchronize(st));
+  unsigned h = 0;
+  for (int k = 0; k < sg_module::kSlots; ++k) h |= w[2 * k];
   if (flags) *flags = h;
   if (h & 1u) return fail(SG_EUNREACHABLE, "point classified into an unreachable sigma entry");
   return SG_OK;
@@ -1045,23 +1080,43 @@ static int launch_binned(sg_module* m, const sg_volume* v, const void* xs, int64
       if (r != CUDA_SUCCESS) return fail(SG_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     }
   }
-  unsigned* err = m->d_err;
+  unsigned* err = nullptr;
+  std::unique_lock<std::mutex> slot_lock;
+  int slot = 0;
+  int rc = acquire_slot(m, st, false, slot_lock, &slot, &err);
+  if (rc) return rc;
   const void* sp = sorted;
   const void* stp = starts;
   const void* itp = items;
   void* args[] = {(void*)&sp, (void*)&stp, (void*)&itp, (void*)&out, (void*)&grad, (void*)&dbg,
                   (void*)&err, (void*)&cs, (void*)&tm};
-  int rc = timed_launch(m, (const void*)m->kernel, dim3((unsigned)max_items), dim3(in.block), args,
-                        (size_t)in.smem_bytes, st);
+  rc = timed_launch(m, (const void*)m->kernel, dim3((unsigned)max_items), dim3(in.block), args,
+                    (size_t)in.smem_bytes, st);
+  if (rc) return rc;
+  rc = release_slot(m, slot, st);
   if (rc) return rc;
   CU(cudaEventRecord(m->bin_done, st));
-  return SG_OK;
   return SG_OK;
 }
 
 static int launch(sg_module* m, const sg_volume* v, const void* xs, int64_t n, void* out,
                   void* grad, int32_t* dbg, cudaStream_t st) {
   if (n <= 0) return SG_OK;
+  // the query sort (binned and presort modules) keeps 32-bit query indices, bin starts and
+  // cursors: batches of 2^30 or more queries are evaluated in 2^30-query pieces
+  const int64_t kSortMax = (int64_t)1 << 30;
+  if ((m->info.mode == SG_MODE_BINNED || m->info.presort) && n > kSortMax) {
+    const size_t es = dtype_size(m->info.dtype);
+    const int s = m->info.dim;
+    for (int64_t q0 = 0; q0 < n; q0 += kSortMax) {
+      const int64_t cnt = std::min(kSortMax, n - q0);
+      int rc = launch(m, v, (const char*)xs + (size_t)q0 * s * es, cnt, (char*)out + (size_t)q0 * es,
+                      grad ? (char*)grad + (size_t)q0 * s * es : nullptr,
+                      dbg ? dbg + (size_t)q0 * m->info.ncosets * (s + 1) : nullptr, st);
+      if (rc) return rc;
+    }
+    return SG_OK;
+  }
   if (m->info.mode == SG_MODE_BINNED) return launch_binned(m, v, xs, n, out, grad, dbg, st);
   std::unique_lock<std::mutex> presort_lock;
   if (m->info.presort) {
@@ -1078,7 +1133,7 @@ static int launch(sg_module* m, const sg_volume* v, const void* xs, int64_t n, v
   SgCosets cs{};
   for (int c = 0; c < v->ncosets; ++c) cs.base[c] = v->origin[c];
   long long nn = (long long)n;
-  unsigned* err = m->d_err;
+  unsigned* err = nullptr;
   void* args[] = {(void*)&xs, (void*)&nn, (void*)&out, (void*)&grad, (void*)&dbg, (void*)&err,
                   (void*)&cs};
   long long per_block = (long long)m->info.block * m->info.queries_per_thread;
@@ -1105,10 +1160,15 @@ static int launch(sg_module* m, const sg_volume* v, const void* xs, int64_t n, v
     cap = (long long)sms * occ;
   }
   grid = std::min(grid, cap);
-  if (m->info.smem_bytes > 0 && m->info.mode == SG_MODE_DIRECT)
-    CU(cudaMemsetAsync(m->d_err + 1, 0, sizeof(unsigned), st));   // sorted kernels' tile counter
-  int rc = timed_launch(m, (const void*)m->kernel, dim3((unsigned)grid), dim3(m->info.block), args,
-                        (size_t)std::max(0, m->info.smem_bytes), st, v->alloc, v->bytes);
+  std::unique_lock<std::mutex> slot_lock;
+  int slot = 0;
+  // sorted kernels claim their tiles from the slot's counter
+  int rc = acquire_slot(m, st, m->info.smem_bytes > 0, slot_lock, &slot, &err);
+  if (rc) return rc;
+  rc = timed_launch(m, (const void*)m->kernel, dim3((unsigned)grid), dim3(m->info.block), args,
+                    (size_t)std::max(0, m->info.smem_bytes), st, v->alloc, v->bytes);
+  if (rc) return rc;
+  rc = release_slot(m, slot, st);
   if (rc) return rc;
   if (m->info.presort) CU(cudaEventRecord(m->bin_done, st));
   return SG_OK;
@@ -1130,7 +1190,7 @@ int sg_render(sg_module* m, const sg_volume* v, const float* rays, int64_t npix,
   for (int c = 0; c < v->ncosets; ++c) cs.base[c] = v->origin[c];
   long long nn = (long long)npix;
   int st = steps;
-  unsigned* err = m->d_err;
+  unsigned* err = nullptr;
   void* args[] = {(void*)&rays, (void*)&nn, (void*)&rgba, (void*)&tf, (void*)&st, (void*)&err,
                   (void*)&cs};
   int sms = 148;
@@ -1145,11 +1205,17 @@ int sg_render(sg_module* m, const sg_volume* v, const float* rays, int64_t npix,
         occ < 1)
       occ = 1;
     grid = std::min((nn + 127) / 128, (long long)sms * occ);
-    CU(cudaMemsetAsync(m->d_err + 1, 0, sizeof(unsigned), (cudaStream_t)stream));   // block counter
   }
-  return timed_launch(m, (const void*)m->kernel, dim3((unsigned)grid), dim3(m->info.block), args,
-                      (size_t)std::max(0, m->info.smem_bytes), (cudaStream_t)stream, v->alloc,
-                      v->bytes);
+  std::unique_lock<std::mutex> slot_lock;
+  int slot = 0;
+  // the psi-sorted renderer claims its ray blocks from the slot's counter
+  rc = acquire_slot(m, (cudaStream_t)stream, m->info.smem_bytes > 0, slot_lock, &slot, &err);
+  if (rc) return rc;
+  rc = timed_launch(m, (const void*)m->kernel, dim3((unsigned)grid), dim3(m->info.block), args,
+                    (size_t)std::max(0, m->info.smem_bytes), (cudaStream_t)stream, v->alloc,
+                    v->bytes);
+  if (rc) return rc;
+  return release_slot(m, slot, (cudaStream_t)stream);
 }
 
 int sg_eval(sg_module* m, const sg_volume* v, const void* xs, int64_t n, void* out, void* grad,

@@ -51,7 +51,9 @@ COEFFS = ("imm", "lut", "table")
 class GenConfig:
     """Reference fields (codegen.py:38-46) + B200 kernel-variant knobs."""
     params: ScheduleParams
-    float_width: str = F32
+    # None -> the reference's default (f64, codegen.py:38-46) for direct-mode kernels; the
+    # f32-only execution modes (binned / sorted / render, pack=2) default to f32
+    float_width: str | None = None
     unroll_cosets: bool = True
     form: str = "horner"
     coeffs: str = "imm"
@@ -75,6 +77,9 @@ class GenConfig:
     presort: int = 0             # sorted: bin edge (cells) of a locality pre-sort of the queries (0 = off)
 
     def __post_init__(self):
+        if self.float_width is None:
+            object.__setattr__(self, "float_width",
+                               F64 if (self.mode == "direct" and self.pack == 1) else F32)
         if self.float_width not in (F64, F32):
             raise ValueError(f"float width must be f64 or f32, not {self.float_width!r}")
         if self.form not in FORMS:
@@ -151,6 +156,11 @@ class Tables:
     uniform_psi: bool
     affine: list | None     # per sub: (A int s x s, b int s) with pi_sub[j] = A ref[j] + b
     ref_stencil: list       # n x s
+    n_psi: list = None      # K: stencil size of each reference polynomial (n = the largest)
+
+    @property
+    def uniform_n(self):
+        return len(set(self.n_psi)) == 1
 
 
 def _solve_affine(ref, sten, s):
@@ -223,11 +233,16 @@ def derive_tables(space: SplineSpace) -> Tables:
     ref = stencils[0]
     aff = []
     for st in stencils:
-        r = _solve_affine(ref, st, s)
+        r = _solve_affine(ref, st, s) if len(st) == len(ref) else None
         if r is None:
             aff = None
             break
         aff.append(r)
+    # per reference polynomial: its stencil size (higher-order Voronoi splines carry
+    # per-polynomial stencils; every sub-region of one polynomial has the same size)
+    n_psi = [0] * len(space.ref_polys)
+    for sb in subs:
+        n_psi[sb.psi_index] = len(sb.stencil)
     P = space.indexer.modulus
     Q = len(space.planes)
     return Tables(
@@ -238,7 +253,7 @@ def derive_tables(space: SplineSpace) -> Tables:
         transforms=transforms, tshift=tshift, stencils=stencils, psi=psi, halo=halo,
         uniform_T=len(set(transforms)) == 1, uniform_tp=len(set(tshift)) == 1,
         uniform_stencil=len({tuple(x) for x in stencils}) == 1, uniform_psi=len(set(psi)) == 1,
-        affine=aff, ref_stencil=ref)
+        affine=aff, ref_stencil=ref, n_psi=n_psi)
 
 
 def plane_families(t: Tables) -> dict:
@@ -485,11 +500,10 @@ def _table_bytes(space, t: Tables, cfg) -> int:
 
 def _chunk_trees(space, cfg, t: Tables):
     """Per reference polynomial: per chunk, the tree to evaluate (or None)."""
-    n = t.n
     m = cfg.params.group_size
     out = []
-    for rp in space.ref_polys:
-        cs = group_polynomial(rp.poly, m, range(n))
+    for i, rp in enumerate(space.ref_polys):
+        cs = group_polynomial(rp.poly, m, range(t.n_psi[i]))
         trees = []
         for poly, block in cs.chunks:
             if not poly:
@@ -574,6 +588,12 @@ def generate(space, config: GenConfig | None = None, extents=None,
     if sorted_:
         if cfg.float_width != F32 or s > 3:
             raise ValueError("sorted mode supports f32 kernels of dimension <= 3")
+        # per-tile psi counters live in a 32-entry shared array (one warp scans them), and
+        # pair keys pack (rank | sub << 16) into an int
+        if t.K > 32:
+            raise ValueError(f"sorted mode supports at most 32 reference polynomials, not {t.K}")
+        if t.nsub >= 1 << 15:
+            raise ValueError(f"sorted mode supports fewer than 32768 sub-regions, not {t.nsub}")
         if not cfg.unroll_cosets:
             raise ValueError("sorted mode unrolls the coset loop")
         # per (query, coset) pair: record (u, base) 16 B + order 4 B + key/result 4 B
@@ -674,11 +694,24 @@ def generate(space, config: GenConfig | None = None, extents=None,
             sym_gtrees = [[horner_factorize(f.poly.differentiate(a)) if f is not None
                            and f.poly.differentiate(a) else None for a in range(t.s)]
                           if f is not None else None for f in symforms]
-    plans = [schedule_pipeline(group_polynomial(space.ref_polys[sb.psi_index].poly,
-                                                cfg.params.group_size, range(t.n)), cfg.params)
-             for sb in space.subregions]
-    plan = plans[0]
-    assert all(p.steps == plan.steps for p in plans), "plans differ across sub-regions"
+    # one (m, d) plan per reference polynomial (codegen.py:332-356); with per-polynomial
+    # stencil sizes the plans differ, and a dispatch that evaluates several polynomials on
+    # one fetched stencil (predicated) fetches all n sites first
+    psi_plans = [schedule_pipeline(group_polynomial(rp.poly, cfg.params.group_size,
+                                                    range(t.n_psi[i])), cfg.params)
+                 for i, rp in enumerate(space.ref_polys)]
+    plan = psi_plans[0]
+    # every site of the largest stencil, chunked like a polynomial of n symbols: chunk b of
+    # any polynomial only uses symbols of block b, so all of them can follow this plan
+    plan_all = plan if t.uniform_n else schedule_pipeline(
+        group_polynomial(Poly(s, {}), cfg.params.group_size, range(t.n)), cfg.params)
+
+    def plan_for(psis):
+        return psi_plans[psis[0]] if len(psis) == 1 else plan_all
+    if t.uniform_n:
+        assert all(p.steps == plan.steps for p in psi_plans), "plans differ across sub-regions"
+    elif pack2 or cfg.prefetch:
+        raise ValueError("pack=2 / prefetch need one stencil size for every sub-region")
     refetch = cfg.params.refetch_tables
 
     head = []
@@ -724,6 +757,13 @@ def generate(space, config: GenConfig | None = None, extents=None,
                     q |= ((1 << c_) - 1) << b0
                 tab_r.append(t.sigma[q % t.modulus] if (t.compress or q < len(t.sigma)) else -1)
             radix = strides_r
+    # sign vectors: 32-bit masks, 64-bit when more than 32 planes cross the cell (an
+    # extension of the reference's 32-plane limit, model.validate_space); the radix index
+    # is always small
+    wide = len(t.planes) > 32 and radix is None
+    if len(t.planes) > 64:
+        raise ValueError("at most 64 BSP planes")
+    QT, QS, QO = ("unsigned long long", "ull", "1ull") if wide else ("unsigned", "u", "1u")
     if use_sigma and not sigma_global and radix is None:
         smem.append(("sg_sigma", "short" if _sigma_short(t) else "int", list(t.sigma)))
     tq = s == 3 and fw == F32 and not (t.uniform_T and t.uniform_tp)
@@ -1217,10 +1257,10 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 if radix is not None:
                     L(f"qq += (unsigned)({cnt} * {radix[nrm]});")
                 else:
-                    L(f"qq |= ((1u << {cnt}) - 1u) << {b0};")
+                    L(f"qq |= (({QO} << {cnt}) - {QO}) << {b0};")
                 continue
             D = int(off * 2 ** FIX)
-            L(f"qq |= ({idot(nrm)} >= {D}) ? {1 << i}u : 0u;")
+            L(f"qq |= ({idot(nrm)} >= {D}) ? {1 << i}{QS} : 0{QS};")
 
     def emit_coset(l, dyn, phase="all"):
         """Body for coset `l` (int) or the loop variable `l` (dyn=True).
@@ -1256,7 +1296,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
             # queries outside [2^-7, E) (tiny, negative, beyond the box) bit-identically
             for d in range(s):
                 L(f"long long kk{d}; float xff{d};" + (f" int kwv{d};" if wrap_ext else ""))
-            L("unsigned qq = 0u;")
+            L(f"{QT} qq = 0{QS};")
             L("if (fast_) {")
             em.indent += "  "
             emit_int_select(l, rounding, wrap_ext)
@@ -1310,7 +1350,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
             L(f"const double xc{d} = __dsub_rn(xl{d}, (double)k{d});")
         # ---- membership (codegen.py:230-250; oracle dot = left-to-right)
         if space.planes:
-            L("unsigned q = 0u;")
+            L(f"{QT} q = 0{QS};")
             dots = {}   # one fp64 dot product per distinct normal (planes share families)
             fam_done = set()
             counted = families
@@ -1333,7 +1373,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
                     if radix is not None:
                         L(f"q += (unsigned)({cnt} * {radix[nrm]});")
                     else:
-                        L(f"q |= ((1u << {cnt}) - 1u) << {b0};")
+                        L(f"q |= (({QO} << {cnt}) - {QO}) << {b0};")
                     continue
                 nz = [(e, w) for e, w in enumerate(nrm) if w != 0]
                 if off == 0 and len(nz) == 2 and all(abs(w) == 1 for _, w in nz):
@@ -1342,7 +1382,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
                     (ea, wa), (eb, wb) = nz
                     lhs = f"xc{ea}" if wa == 1 else f"(-xc{ea})"
                     rhs = f"(-xc{eb})" if wb == 1 else f"xc{eb}"
-                    L(f"q |= ({lhs} >= {rhs}) ? {1 << i}u : 0u;")
+                    L(f"q |= ({lhs} >= {rhs}) ? {1 << i}{QS} : 0{QS};")
                     continue
                 if nrm not in dots:
                     acc = None
@@ -1355,7 +1395,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
                         acc = term if acc is None else f"__dadd_rn({acc}, {term})"
                     dots[nrm] = f"dn{len(dots)}"
                     L(f"const double {dots[nrm]} = {acc or '0.0'};")
-                L(f"q |= ({dots[nrm]} >= {dlit(off)}) ? {1 << i}u : 0u;")
+                L(f"q |= ({dots[nrm]} >= {dlit(off)}) ? {1 << i}{QS} : 0{QS};")
         if isel:
             for d in range(s):
                 L(f"kk{d} = k{d}; xff{d} = (float)xc{d};")
@@ -1370,12 +1410,12 @@ def generate(space, config: GenConfig | None = None, extents=None,
             for d in range(s):
                 L(f"const long long k{d} = kk{d};")
             if space.planes:
-                L("unsigned q = qq;")
+                L(f"{QT} q = qq;")
         if space.planes:
             if radix is not None:
                 L("int sub = __ldg(&sg_sigma_r[q]);")
             elif t.compress:
-                L(f"q = q % {P}u;")
+                L(f"q = q % {P}{QS};")
             if radix is not None:
                 pass
             elif sigma_global:
@@ -1390,7 +1430,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
                     L("if (sub < 0) { atomicOr(err, 1u); sub = 0; }")
                 else:
                     bad = [qq for qq, x in enumerate(t.sigma) if x < 0]
-                    cond = " || ".join(f"q == {qq}u" for qq in bad)
+                    cond = " || ".join(f"q == {qq}{QS}" for qq in bad)
                     L(f"if ({cond}) atomicOr(err, 1u);")
         else:
             L("const int sub = 0;")
@@ -1513,7 +1553,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
         def run_plan_sym(psis, tag):
             """All fetches in plan order, then per psi the symmetry-mixed symbols and
             one Horner evaluation of psi'(v, s) (form "sym")."""
-            for step in plan.steps:
+            for step in plan_for(psis).steps:
                 if step.kind == FETCH:
                     j = step.index
                     L(fetch_line(j, tag))
@@ -1577,7 +1617,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
             accs = {i: None for i in psis}
             u = None
             nchunk = 0
-            for step in plan.steps:
+            for step in plan_for(psis).steps:
                 if step.kind == FETCH:
                     j = step.index
                     L(fetch_line(j, tag))
@@ -1585,6 +1625,8 @@ def generate(space, config: GenConfig | None = None, extents=None,
                     if u is None or refetch:
                         u = emit_u(f"{tag}_{nchunk}" if refetch else tag)
                     for i in psis:
+                        if step.index >= len(trees[i]):
+                            continue
                         tree = trees[i][step.index]
                         if tree is None:
                             continue
@@ -1666,12 +1708,12 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 L(f"{T} g{m} = ({T})0;")
             u = None
             nchunk = 0
-            for step in plan.steps:
+            for step in plan_all.steps:
                 if step.kind == FETCH:
                     j = step.index
                     L(fetch_line(j, ""))
                 elif step.kind == COMPUTE:
-                    for j in plan.blocks[step.index]:
+                    for j in plan_all.blocks[step.index]:
                         for q in range(nmp // w):
                             L(f"{{ const {vec} a_ = Arow[{(j * tab['nq'] + q) * t.K}]; " + " ".join(
                                 f"g{q * w + r} = a_.{comps[r]} * c{j} + g{q * w + r};" for r in range(w)) + " }")

@@ -223,7 +223,7 @@ class Module:
 
     def status(self, stream=None):
         f = ctypes.c_uint32()
-        _check(lib().sg_module_status(self.handle, _stream_ptr(stream), ctypes.byref(f)))
+        _check(lib().sg_module_status(self.handle, _stream_ptr(stream, self.device), ctypes.byref(f)))
         return f.value
 
     def __del__(self):
@@ -268,7 +268,7 @@ class Volume:
             pad = (ctypes.c_int64 * (len(arrs) * self.dim))(*[e for row in padded for e in row])
         _check(lib().sg_volume_create(device, self.dim, len(arrs), ext, halo, pad,
                                       SG_F32 if np_dtype == np.float32 else SG_F64, ptrs,
-                                      int(on_dev), _stream_ptr(stream), ctypes.byref(h)))
+                                      int(on_dev), _stream_ptr(stream, device), ctypes.byref(h)))
         self.handle = h
         self.ncosets = len(arrs)
 
@@ -285,12 +285,14 @@ class Volume:
             self.handle = None
 
 
-def _stream_ptr(stream):
+def _stream_ptr(stream, device=None):
+    """cudaStream_t of `stream`; None = torch's current stream on `device` (the module's
+    device, not whatever device happens to be current)."""
     if stream is None:
         try:
             import torch
             if torch.cuda.is_available():
-                return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+                return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
         except Exception:  # pragma: no cover
             pass
         return ctypes.c_void_p(0)
@@ -300,20 +302,26 @@ def _stream_ptr(stream):
 
 
 def eval_device(module: Module, volume: Volume, xs, out, grad=None, dbg=None, stream=None):
-    """Launch on torch device tensors (async on the current torch stream)."""
+    """Launch on torch device tensors (async on the current torch stream of the module's
+    device).  Every tensor must live on that device: a host pointer handed to the kernel
+    would fault and poison the CUDA context, so it is rejected here."""
+    for name, t in (("xs", xs), ("out", out), ("grad", grad), ("dbg", dbg)):
+        if t is not None and (not t.is_cuda or t.device.index != module.device):
+            raise SplineGpuError(SG_EINVAL, f"{name} must be a CUDA tensor on cuda:{module.device}, "
+                                            f"not {t.device}")
     n = xs.shape[0]
     _check(lib().sg_eval(module.handle, volume.handle, ctypes.c_void_p(xs.data_ptr()), n,
                          ctypes.c_void_p(out.data_ptr()),
                          ctypes.c_void_p(grad.data_ptr() if grad is not None else 0),
                          ctypes.c_void_p(dbg.data_ptr() if dbg is not None else 0),
-                         _stream_ptr(stream)))
+                         _stream_ptr(stream, module.device)))
 
 
 def render_device(module: Module, volume: Volume, rays, steps: int, tf, rgba, stream=None):
     """Fused ray-march + reconstruction + compositing (render-mode modules, sg_render)."""
     _check(lib().sg_render(module.handle, volume.handle, ctypes.c_void_p(rays.data_ptr()),
                            rays.shape[0], int(steps), ctypes.c_void_p(tf.data_ptr()),
-                           ctypes.c_void_p(rgba.data_ptr()), _stream_ptr(stream)))
+                           ctypes.c_void_p(rgba.data_ptr()), _stream_ptr(stream, module.device)))
 
 
 def eval_host(module: Module, volume: Volume, xs: np.ndarray, out: np.ndarray,

@@ -32,7 +32,8 @@ def test_capi_demo_builds_with_gcc(tmp_path):
 def test_capi_demo_matches_oracle(tmp_path, name, mode):
     from paper_2102_08518_b200 import GenConfig, ScheduleParams, generate
     space, ospace, z, arrays = load_golden(name)
-    prog = generate(space, GenConfig(ScheduleParams(1, space.stencil_size), mode=mode),
+    prog = generate(space, GenConfig(ScheduleParams(1, space.stencil_size), mode=mode,
+                                     float_width="f32"),
                     arrays[0].shape)
     (tmp_path / "k.cu").write_text(prog.source)
     fields = [prog.dim, prog.ncosets, prog.block, prog.halo, 1 if prog.mode == "binned" else 0,

@@ -27,6 +27,7 @@ def _cfg(space, spec):
     spec = dict(spec)
     n = space.stencil_size
     mode = spec.pop("params_mode", "predicated")
+    spec.setdefault("float_width", "f32")
     return GenConfig(params=ScheduleParams(1, n, mode), **spec)
 
 
@@ -36,6 +37,10 @@ def test_variant_generates_and_compiles(name, variant):
     space, _, _, arrays = load_golden(name)
     ext = arrays[0].shape
     cfg = _cfg(space, VARIANTS[variant])
+    if variant.startswith("pack2") and not space.uniform_stencils:
+        with pytest.raises(ValueError, match="one stencil size"):
+            generate(space, cfg, ext)
+        return
     a = generate(space, cfg, ext)
     b = generate(space, cfg, ext)
     assert a.source == b.source

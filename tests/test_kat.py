@@ -22,6 +22,7 @@ def _dbg_eval(name, xs, **kw):
     import torch
     from paper_2102_08518_b200 import Evaluator, GenConfig, ScheduleParams
     space, _, _, arrays = load_golden(name)
+    kw.setdefault("float_width", "f32")
     ev = Evaluator(space, arrays, GenConfig(ScheduleParams(1, space.stencil_size), dbg=True, **kw))
     out, _, dbg = ev(torch.tensor(xs, dtype=torch.float32).cuda())
     return out.cpu().numpy(), dbg.cpu().numpy()
@@ -68,6 +69,7 @@ def _values(name, xs, **kw):
     mode = kw.pop("branch", "predicated")
     refetch = kw.pop("refetch", False)
     data = kw.pop("arrays", arrays)
+    kw.setdefault("float_width", "f32")
     cfg = GenConfig(ScheduleParams(md[0], md[1], mode, refetch), **kw)
     ev = Evaluator(space, data, cfg)
     return ev(torch.as_tensor(np.asarray(xs, np.float32)).cuda()).cpu().numpy()

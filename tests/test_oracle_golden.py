@@ -49,6 +49,8 @@ def test_oracle_selection_bit_exact(name, which):
 def test_reference_generated_code_agrees(name):
     """The reference's own f64 generated program agrees with its oracle (1e-9)."""
     space, z, arrays = _load(name)
+    if "uniform_interp_f64" not in z:
+        pytest.skip("extension space: the reference generator refuses it (make_golden.py)")
     want = z["uniform_value"]
     got = z["uniform_interp_f64"]
     assert np.all(np.abs(got - want) <= 1e-12 + 1e-9 * np.maximum(abs(got), abs(want)))

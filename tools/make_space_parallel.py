@@ -4,6 +4,7 @@
     python tools/make_space_parallel.py bcc_voronoi3 [workers]
 """
 import multiprocessing as mp
+import pickle
 import sys
 import time
 from pathlib import Path
@@ -19,6 +20,8 @@ from paper_2102_08518_b200.partone.voronoi import BCC_VORONOI_GENS, FCC_VORONOI_
 SPECS = {
     "bcc_voronoi3": (lambda: voronoi_spline(BCC_VORONOI_GENS, 3), BCC_COSETS, BCC_GEN, (8, 8, 8)),
     "fcc_voronoi3": (lambda: voronoi_spline(FCC_VORONOI_GENS, 3), FCC_COSETS, FCC_GEN, (6, 6, 6)),
+    "bcc_voronoi4": (lambda: voronoi_spline(BCC_VORONOI_GENS, 4), BCC_COSETS, BCC_GEN, (8, 8, 8)),
+    "fcc_voronoi4": (lambda: voronoi_spline(FCC_VORONOI_GENS, 4), FCC_COSETS, FCC_GEN, (8, 8, 8)),
 }
 _P = None
 
@@ -44,8 +47,13 @@ def main():
     p.orbits()
     p.reps_all = list(p.reps)
     _P = p
-    with mp.get_context("fork").Pool(workers) as pool:
-        res = sorted(pool.map(_fit_one, range(len(p.reps_all)), chunksize=1))
+    ck = Path(f"/tmp/{name}_fits.pkl")
+    if ck.exists():
+        res = pickle.loads(ck.read_bytes())
+    else:
+        with mp.get_context("fork").Pool(workers) as pool:
+            res = sorted(pool.map(_fit_one, range(len(p.reps_all)), chunksize=1))
+        ck.write_bytes(pickle.dumps(res))
     p.reps = p.reps_all
     p.ref_polys = [r[1] for r in res]
     p.ref_stencils = [r[2] for r in res]
