@@ -793,7 +793,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
             vals = []
             for sten in t.stencils:
                 row = [sum(site[d] * st[d] for d in range(s)) for site in sten]
-                vals += row + [0] * (npad - t.n)
+                vals += row + [0] * (npad - len(row))
             smem.append((f"sg_off{g}", "int", vals))
     if not t.uniform_psi and t.K > 1:
         smem.append(("sg_psi", "int", list(t.psi)))
