@@ -59,6 +59,14 @@ CONFIGS = {
     "c4v": dict(space="fcc_voronoi2", extents=(161, 161, 161), queries=1 << 26, kind="uniform",
                 grad=True, scaling="weak", variant=dict(mode="direct", coeffs="table", block=128),
                 desc="FCC Voronoi spline (order 2), 4x161^3, 2^26 uniform, value + gradient"),
+    "c4v3": dict(space="fcc_voronoi3", extents=(161, 161, 161), queries=1 << 26, kind="uniform",
+                 grad=True, scaling="weak", variant=dict(mode="sorted", coeffs="imm", block=512, radix=1),
+                 desc="FCC Voronoi spline (order 3, the paper's FCC case), 4x161^3, 2^26 uniform, "
+                      "value + gradient"),
+    "c3v3": dict(space="bcc_voronoi3", extents=(203, 203, 203), queries=1 << 26, kind="rays",
+                 rays=(512, 512, 256), grad=False, scaling="weak",
+                 variant=dict(mode="sorted", coeffs="imm", block=512, radix=1),
+                 desc="BCC Voronoi spline (order 3, the paper's K=7 case), 2x203^3, 2^26 ray-ordered"),
     "c5u": dict(space="bcc_voronoi2", extents=(406, 406, 406), queries=1 << 30, kind="uniform",
                 grad=False, scaling="strong",
                 variant=dict(mode="binned", stage="l1", block=256, bin=136, coeffs="imm"),
@@ -248,6 +256,7 @@ def cpu_baseline(space_name, arrays_f32, xs_f32, budget_s=15.0, shard=1 << 14, p
         pool.join()
     n = nshards * shard
     return {"value": n / wall / 1e9, "unit": "Grecon/s", "cores": cores, "kind": "port",
+            "cpu_model": cpu_model(), "rate_1core": rate1 / 1e9,
             "sample": f"{n} of the configuration's queries ({nshards} shards of {shard}), "
                       f"oracle/refeval.reference_eval_batch (numpy f64, restatement of "
                       f"splinegen.oracle.reference_eval_batch) on {cores} processes, "
@@ -298,6 +307,41 @@ def make_inputs(cfg_name, rank, device, world=1):
     return space, arrays, xs
 
 
+def config_dict(cfg_name, world):
+    """The line's `config` object -- built identically by both arms (ours and --impl
+    reference), so the driver can match them."""
+    from paper_2102_08518_b200 import load_fixture
+    c = CONFIGS[cfg_name]
+    sp = load_fixture(c["space"])
+    lo, hi = query_range(cfg_name, 0, world)
+    n = hi - lo
+    d = {"workload": cfg_name + ": " + c["desc"], "space": c["space"],
+         "extents": list(c["extents"]), "cosets": sp.ncosets, "query_kind": c["kind"]}
+    if c["kind"] == "render":
+        w, h, steps = c["rays"]
+        d.update({"image": [w, h], "samples_per_ray": steps, "samples_per_gpu": w * h * steps,
+                  "shading": c["grad"], "parallelism": f"full image per GPU x{world}",
+                  "l2": "no query/result streams: samples are generated and consumed in registers"})
+        return d
+    d.update({"queries_per_gpu": n, "gradient": c["grad"],
+              "parallelism": f"query shards x{world}, volume replicated",
+              "l2": "L2 flushed between steps" if n * sp.dim * 4 < 2 * 126e6
+              else "query stream > L2 (126 MB); volume L2-resident by design"
+              if 4 * sp.ncosets * math.prod(c["extents"]) < 100e6
+              else "query stream and volume > L2 (126 MB)"})
+    return d
+
+
+def cpu_model():
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def roofline(cfg_name, falg, n, eval_kernel_ms, step_ms, pk):
     """roofline block of the bench line for the dominant kernel (sg_eval_kernel).
 
@@ -309,14 +353,41 @@ def roofline(cfg_name, falg, n, eval_kernel_ms, step_ms, pk):
     ncu on the same launch (profiles/ncu_<config>.json)."""
     if not falg:
         return None
+    from paper_2102_08518_b200 import load_fixture
+    c = CONFIGS[cfg_name]
+    sp = load_fixture(c["space"])
+    # SURVEY 8d: T_floor = max(F_alg / P_fp32, B_alg / BW), BW = HBM when the coset
+    # volume exceeds L2.  B_alg = 4 B per coefficient gather (mean stencil size over the
+    # sub-regions' polynomials) + the query and result streams (+ gradient)
+    nbar = float(np.mean([len(sb.stencil) for sb in sp.subregions]))
+    balg = 4 * nbar * sp.ncosets + 4 * sp.dim + 4 + (4 * sp.dim if c["grad"] else 0)
+    vol_bytes = 4 * sp.ncosets * math.prod(c["extents"])
+    t_fp = falg / (pk["fp32_tflops"] * 1e12)
+    t_hbm = balg / (pk["hbm_gbs"] * 1e9)
+    hbm_block = None
+    if vol_bytes > 126e6 or t_hbm > t_fp:
+        a = balg * n / (eval_kernel_ms / 1e3) / 1e9
+        hbm_block = {"bytes_per_query": round(balg, 1), "achieved": round(a, 1),
+                     "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(a / pk["hbm_gbs"], 4),
+                     "volume_bytes": vol_bytes}
     achieved = falg * n / (eval_kernel_ms / 1e3) / 1e12
-    roof = {"bound": "fp32", "achieved": round(achieved, 3), "peak": round(pk["fp32_tflops"], 2),
-            "unit": "TFLOP/s", "frac": round(achieved / pk["fp32_tflops"], 4), "traffic": None,
+    if hbm_block and t_hbm > t_fp:
+        roof = {"bound": "hbm", "achieved": hbm_block["achieved"], "peak": pk["hbm_gbs"],
+                "unit": "GB/s", "frac": hbm_block["frac"], "traffic": None,
+                "fp32": {"achieved": round(achieved, 3), "peak": round(pk["fp32_tflops"], 2),
+                         "unit": "TFLOP/s", "frac": round(achieved / pk["fp32_tflops"], 4)}}
+    else:
+        roof = {"bound": "fp32", "achieved": round(achieved, 3), "peak": round(pk["fp32_tflops"], 2),
+                "unit": "TFLOP/s", "frac": round(achieved / pk["fp32_tflops"], 4), "traffic": None}
+        if hbm_block:
+            roof["hbm"] = hbm_block
+    roof.update({
             "note": f"F_alg = {falg:g} FP ops/query (reference dynamic count, m=1 d=n branchy; "
                     f"tests/golden/falg.json) x {n} queries / sg_eval_kernel time "
                     f"({eval_kernel_ms:.4f} ms of the {step_ms:.4f} ms step, CUDA events on the "
                     f"launch stream); peak = 148 SM x 128 FP32 lanes x 2 x {pk['sm_max_mhz']:.0f} MHz "
-                    f"({pk['source']} sm_max_mhz)"}
+                    f"({pk['source']} sm_max_mhz); binding roof = max(F_alg / FP32 peak, "
+                    f"B_alg / HBM) per query (SURVEY 8d)"})
     prof = PROFILES / f"ncu_{cfg_name}.json"
     if prof.exists():
         d = json.loads(prof.read_text())
@@ -340,12 +411,11 @@ def roofline(cfg_name, falg, n, eval_kernel_ms, step_ms, pk):
         # one 4-B read per stencil site and coset)
         from paper_2102_08518_b200 import load_fixture
         c = CONFIGS[cfg_name]
-        sp = load_fixture(c["space"])
-        gbytes = 4 * sp.stencil_size * sp.ncosets
+        gbytes = 4 * nbar * sp.ncosets
         l2 = json.loads(l2p.read_text()).get("l2_gbs")
         if l2:
             a = gbytes * n / (eval_kernel_ms / 1e3) / 1e9
-            roof["l2_gathers"] = {"bytes_per_query": gbytes, "achieved": round(a, 1), "peak": l2,
+            roof["l2_gathers"] = {"bytes_per_query": round(gbytes, 1), "achieved": round(a, 1), "peak": l2,
                                   "unit": "GB/s", "frac": round(a / l2, 4),
                                   "peak_source": "profiles/r01_l2_bandwidth.json"}
     return roof
@@ -478,12 +548,7 @@ def run_ours(args, rank, world, device):
         "value": round(value, 4), "unit": "Grecon/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(kernel_ms, 4), "higher_is_better": True,
         "scaling": c["scaling"], "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": args.config + ": " + c["desc"], "space": c["space"],
-                   "extents": list(c["extents"]), "cosets": space.ncosets,
-                   "queries_per_gpu": n, "query_kind": c["kind"],
-                   "parallelism": f"query shards x{world}, volume replicated",
-                   "l2": "L2 flushed between steps" if l2_flush is not None
-                   else "query stream > L2 (126 MB); volume L2-resident by design"},
+        "config": config_dict(args.config, world),
         "e2e": {"value": round(e2e_value, 4), "unit": "Grecon/s",
                 "h2d_bytes_per_step": n * space.dim * 4,
                 "d2h_bytes_per_step": n * 4 * (1 + (space.dim if grad is not None else 0)),
@@ -572,11 +637,7 @@ def run_render(args, rank, world, device):
         "value": round(value, 4), "unit": "Grecon/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": True,
         "scaling": c["scaling"], "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": args.config + ": " + c["desc"], "space": c["space"],
-                   "extents": list(c["extents"]), "cosets": space.ncosets, "image": [w, h],
-                   "samples_per_ray": steps, "samples_per_gpu": n, "shading": c["grad"],
-                   "parallelism": f"full image per GPU x{world}",
-                   "l2": "no query/result streams: samples are generated and consumed in registers"},
+        "config": config_dict(args.config, world),
         "e2e": {"value": round(e2e_value, 4), "unit": "Grecon/s",
                 "h2d_bytes_per_step": int(r.rays_np.nbytes), "d2h_bytes_per_step": w * h * 16,
                 "steps": e2e_steps, "path": "ray table H2D (pinned), sg_render, rgba D2H"},
@@ -615,7 +676,9 @@ def run_reference(args, rank, world):
     arrays = [rng.random(c["extents"]).astype(np.float32) for _ in range(space.ncosets)]
     if c["kind"] == "render":
         return run_reference_render(args, c, space, arrays)
-    xs = make_queries(args.config, 0, 1 << 18, "cpu").numpy()
+    # the fixed 2^20-query prefix of the configuration's stream, generated by
+    # the same index-addressable generator the GPU arm uses
+    xs = make_queries(args.config, 0, 1 << 20, "cpu").numpy()
     total_budget = 10.0 * args.cpu_budget       # seconds for the whole run (default 150 s)
     per_step = total_budget / (args.steps + args.warmup)
     cores = len(os.sched_getaffinity(0))
@@ -638,8 +701,7 @@ def run_reference(args, rank, world):
         "value": v, "unit": "Grecon/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": None, "higher_is_better": True, "scaling": c["scaling"], "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config + ": " + c["desc"], "space": c["space"],
-                   "extents": list(c["extents"]), "query_kind": c["kind"]},
+        "config": config_dict(args.config, world),
         "cpu_baseline": {**vals[-1], "value": v},
         "e2e": {"value": v, "unit": "Grecon/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -671,8 +733,9 @@ def run_reference_render(args, c, space, arrays):
             "value": v, "unit": "Grecon/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": None, "higher_is_better": True, "scaling": c["scaling"], "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config + ": " + c["desc"], "space": c["space"]},
+            "config": config_dict(args.config, 1),
             "cpu_baseline": {"value": v, "unit": "Grecon/s", "cores": 1, "kind": "port",
+                             "cpu_model": cpu_model(),
                              "sample": f"{npx} rays x {steps} samples per step, oracle/render.py"},
             "e2e": {"value": v, "unit": "Grecon/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 

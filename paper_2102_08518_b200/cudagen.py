@@ -75,6 +75,9 @@ class GenConfig:
     radix: int = 0               # 1: sub-region via a mixed-radix index of the plane-family counts
     rank: str = "match"          # sorted: rank in the psi class by "match" (warp-aggregated) | "atomic"
     presort: int = 0             # sorted: bin edge (cells) of a locality pre-sort of the queries (0 = off)
+    tloop: int = 0               # coeffs="table": 1 = a runtime loop over the stencil sites (code
+                                 # shared by every reference polynomial: no instruction-cache
+                                 # pressure for large polynomials), 0 = fully unrolled
 
     def __post_init__(self):
         if self.float_width is None:
@@ -480,6 +483,9 @@ class CudaProgram:
         return np.float32 if self.float_width == F32 else np.float64
 
 
+DYN_TABLE_MIN = 40 * 1024     # sorted mode: larger shared tables live in dynamic shared memory
+
+
 def _sigma_short(t: Tables) -> bool:
     return all(-32768 <= v < 32768 for v in t.sigma)
 
@@ -601,7 +607,9 @@ def generate(space, config: GenConfig | None = None, extents=None,
         pair_bytes = 36 if cfg.grad else 24
         if cfg.tile == 0:
             tb = _table_bytes(space, t, cfg)
-            room = 110 * 1024 - tb
+            # tables beyond the static limit go to dynamic shared memory beside the pair
+            # records; then one CTA per SM owns the 227 KB
+            room = (110 if tb <= DYN_TABLE_MIN else 210) * 1024 - tb
             tq = max(cfg.block, min(8192, room // (M * pair_bytes)) // cfg.block * cfg.block)
             tq = min(tq, max(cfg.block, 2048 // cfg.block * cfg.block))
             cfg = replace(cfg, tile=tq)
@@ -824,8 +832,10 @@ def generate(space, config: GenConfig | None = None, extents=None,
         smem.append(("sg_A", T, Atab))
         if tab["has_free"]:
             smem.append(("sg_A0", T, A0tab))
-        if 4 * len(Atab) > 96 * 1024:
+        if 4 * len(Atab) > (190 if sorted_ else 96) * 1024:
             raise ValueError("coefficient table too large for shared memory")
+        if not t.uniform_n:
+            smem.append(("sg_npsi", "int", list(t.n_psi)))
 
     lut = []
     if cfg.coeffs == "lut":
@@ -855,6 +865,24 @@ def generate(space, config: GenConfig | None = None, extents=None,
         A(f"__device__ const short sg_sigma_r[{len(tab_r)}] = {{{', '.join(str(v) for v in tab_r)}}};")
     if sigma_global and radix is None:
         A(f"__device__ const int sg_sigma_g[{len(t.sigma)}] = {{{', '.join(str(v) for v in t.sigma)}}};")
+
+    # sorted mode: shared tables beyond the static limit go to dynamic shared memory, after
+    # the tile's pair records (offsets fixed here; sorted_smem adds their bytes)
+    dyn_tables, dyn_bytes = {}, 0
+    if sorted_:
+        elem = {"float": 4, "double": 8, "int": 4, "short": 2}
+        static_b = sum(elem[ct] * len(v) for _n, ct, v in smem)
+        if static_b > DYN_TABLE_MIN:
+            pair_b = M * cfg.tile * (36 if cfg.grad else 24) + (cfg.tile * 4 if presort else 0)
+            off = -(-pair_b // 16) * 16
+            for name, ct, v in sorted(smem, key=lambda e: -elem[e[1]] * len(e[2])):
+                if static_b <= DYN_TABLE_MIN // 4:
+                    break
+                nb = elem[ct] * len(v)
+                dyn_tables[name] = (ct, off)
+                off += -(-nb // 16) * 16
+                static_b -= nb
+            dyn_bytes = off - -(-pair_b // 16) * 16 + (-(-pair_b // 16) * 16 - pair_b)
 
     # ---- kernel -------------------------------------------------------------
     def direct_preamble(pre="  "):
@@ -931,7 +959,8 @@ def generate(space, config: GenConfig | None = None, extents=None,
         return out
 
     # sorted: 2 CTAs / SM by design; render: an explicit bound (ptxas otherwise caps at 48 regs)
-    min_blocks = cfg.min_blocks or (2 if sorted_ else (max(1, 256 // cfg.block) if (render or pack2) else 0))
+    min_blocks = cfg.min_blocks or ((1 if dyn_tables else 2) if sorted_
+                                    else (max(1, 256 // cfg.block) if (render or pack2) else 0))
     lb = f"{cfg.block}, {min_blocks}" if min_blocks else f"{cfg.block}"
     body = []
     B = body.append
@@ -946,13 +975,17 @@ def generate(space, config: GenConfig | None = None, extents=None,
             B(f"    const {T}* __restrict__ xs, long long n, {T}* __restrict__ out, {T}* __restrict__ grad,")
             B("    int* __restrict__ dbg, unsigned* __restrict__ err, SgCosets vol) {")
         for name, ctype, vals in smem:
-            B(f"  __shared__ __align__(16) {ctype} {name}[{len(vals)}];")
+            if name not in dyn_tables:
+                B(f"  __shared__ __align__(16) {ctype} {name}[{len(vals)}];")
+        if sorted_:
+            B("  extern __shared__ __align__(16) unsigned char sg_dyn[];")
+            for name, (ctype, off) in dyn_tables.items():
+                B(f"  {ctype}* {name} = reinterpret_cast<{ctype}*>(sg_dyn + {off});")
         for name, ctype, vals in smem:
             B(f"  for (int i_ = threadIdx.x; i_ < {len(vals)}; i_ += {cfg.block}) {name}[i_] = __ldg(&{name}_c[i_]);")
         if sorted_:
             TQ = cfg.tile
             MP = M * TQ
-            B("  extern __shared__ __align__(16) unsigned char sg_dyn[];")
             B("  float4* sg_rec = reinterpret_cast<float4*>(sg_dyn);")
             # the pair keys (rank | sub << 16) live in the result array until the scatter
             if cfg.grad:
@@ -972,7 +1005,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
             for l in range(M):
                 B(f"  const int coff{l} = (int)((const float*)vol.base[{l}] - (const float*)vol.base[0]);")
             B("  __syncthreads();")
-            sorted_smem = MP * pair_bytes + (TQ * 4 if presort else 0)
+            sorted_smem = MP * pair_bytes + (TQ * 4 if presort else 0) + dyn_bytes
             if presort:
                 # original index of every tile query (the input is the locality-sorted records)
                 B(f"  int* sg_qidx = reinterpret_cast<int*>(sg_dyn + {MP * pair_bytes});")
@@ -1708,7 +1741,27 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 L(f"{T} g{m} = ({T})0;")
             u = None
             nchunk = 0
-            for step in plan_all.steps:
+            if cfg.tloop:
+                # one runtime loop over the polynomial's stencil sites: the same few hundred
+                # instructions serve every reference polynomial (large K x n tables would
+                # otherwise be unrolled into per-polynomial code that thrashes the I-cache);
+                # the next site's coefficient is fetched one iteration ahead
+                if fetch_mode != "table":
+                    raise ValueError("tloop needs per-sub-region offset tables")
+                nsite = (f"sg_npsi[{psi_e}]" if not t.uniform_n else str(t.n))
+                L(f"const int ns_ = {nsite};")
+                rd = (lambda o: f"V[{o}]") if smem_fetch else (lambda o: f"__ldg(V + ({o}))")
+                L(f"{T} cn_ = {rd('base + offt[0]')};")
+                L("#pragma unroll 1")
+                L("for (int j_ = 0; j_ < ns_; ++j_) {")
+                L(f"  const {T} cj_ = cn_;")
+                L(f"  if (j_ + 1 < ns_) cn_ = {rd('base + offt[j_ + 1]')};")
+                L(f"  const {vec}* __restrict__ Aj_ = Arow + j_ * {tab['nq'] * t.K};")
+                for q in range(nmp // w):
+                    L(f"  {{ const {vec} a_ = Aj_[{q * t.K}]; " + " ".join(
+                        f"g{q * w + r} = a_.{comps[r]} * cj_ + g{q * w + r};" for r in range(w)) + " }")
+                L("}")
+            for step in (() if cfg.tloop else plan_all.steps):
                 if step.kind == FETCH:
                     j = step.index
                     L(fetch_line(j, ""))

@@ -91,6 +91,8 @@ def _rat(v, den=1 << 24):
 
 
 class Producer:
+    grid_den = 64   # boundary_q: closed-cell grid step
+
     def __init__(self, phi: BoxSum, cosets, generator, name, rounding="round_nearest",
                  seed=0, verbose=False):
         self.phi = phi
@@ -444,8 +446,32 @@ class Producer:
                     if q in self.q_to_region or q in extra:
                         continue
                     extra[q] = self._adjacent_region(x)
+        # every point of the closed cell on the dyadic grid of step 1/grid_den: covers the
+        # vertices and every segment / 2-D cell of the plane arrangement restricted to the
+        # cell's faces (plane offsets are multiples of 1/4 with small-integer normals, so
+        # those features all carry grid points), where generic sampling can miss a segment
+        # -- e.g. a line of two planes lying inside a face, whose sign vector no interior
+        # region has (order-3 BCC Voronoi)
+        den = self.grid_den
+        g = np.arange(den + 1, dtype=np.float64) / den * float(self.hi - self.lo) + float(self.lo)
+        pts = np.stack(np.meshgrid(*([g] * s), indexing="ij"), axis=-1).reshape(-1, s)
+        bits = np.zeros(len(pts), dtype=np.uint64)
+        for i, (a, o) in enumerate(self.plane_list):
+            av = np.array([float(v) for v in a])
+            bits |= ((pts @ av) >= float(o)).astype(np.uint64) << np.uint64(i)
+        known = set(self.q_to_region) | set(extra)
+        uq, first = np.unique(bits, return_index=True)
+        added = 0
+        for qb, idx in zip(uq.tolist(), first.tolist()):
+            if int(qb) in known:
+                continue
+            x = tuple(F(v).limit_denominator(4 * den) for v in pts[idx])
+            if self.qbits(x) != int(qb):
+                raise RuntimeError("grid sign vector is not exact")
+            extra[int(qb)] = self._adjacent_region(x)
+            added += 1
         self.extra_q = extra
-        self.log(f"{len(extra)} boundary-only sign vectors")
+        self.log(f"{len(extra)} boundary-only sign vectors ({added} from the 1/{den} grid)")
         return extra
 
     def _points_on(self, rows, count):

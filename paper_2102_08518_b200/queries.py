@@ -14,7 +14,6 @@ same global set on its own device (multi-GPU runs see identical work).
 
 from __future__ import annotations
 
-import math
 
 import numpy as np
 
@@ -165,8 +164,3 @@ def make(kind: str, lo: int, hi: int, extents, device, seed: int = 1, **kw):
                     device)
     raise ValueError(kind)
 
-
-def check_sizes(kind, n, **kw):
-    if kind == "rays" and kw["width"] * kw["height"] * kw["steps"] != n:
-        raise ValueError("ray stream size mismatch")
-    return math.prod([1])

@@ -102,6 +102,31 @@ VARIANTS = {
     "chunk8k": dict(chunk=8192),
     "chunk16k": dict(chunk=16384),
     "chunk2k": dict(chunk=2048),
+    "branchy": dict(mode="direct", block=128, branchy=True, coeffs="imm"),
+    "branchy_sym": dict(mode="direct", block=128, branchy=True, form="sym", coeffs="imm"),
+    "direct_table": dict(mode="direct", block=128, coeffs="table"),
+    "srt_imm": dict(mode="sorted", block=512, radix=1, coeffs="imm"),
+    "srt_imm_b256": dict(mode="sorted", block=256, radix=1, coeffs="imm"),
+    "srt_sym": dict(mode="sorted", block=512, radix=1, coeffs="imm", form="sym"),
+    "srt_sym_b256": dict(mode="sorted", block=256, radix=1, coeffs="imm", form="sym"),
+    "srt_table": dict(mode="sorted", block=512, radix=1, coeffs="table"),
+    "tl512": dict(mode="sorted", block=512, radix=1, coeffs="table", tloop=1),
+    "tl256": dict(mode="sorted", block=256, radix=1, coeffs="table", tloop=1),
+    "tl384": dict(mode="sorted", block=384, radix=1, coeffs="table", tloop=1),
+    "tl512_t1024": dict(mode="sorted", block=512, tile=1024, radix=1, coeffs="table", tloop=1),
+    "tl256_t1024": dict(mode="sorted", block=256, tile=1024, radix=1, coeffs="table", tloop=1),
+    "srt_imm_b128": dict(mode="sorted", block=128, radix=1, coeffs="imm"),
+    "srt_imm_b256_t512": dict(mode="sorted", block=256, tile=512, radix=1, coeffs="imm"),
+    "srt_imm_b256_t2048": dict(mode="sorted", block=256, tile=2048, radix=1, coeffs="imm"),
+    "srt_imm_b384": dict(mode="sorted", block=384, radix=1, coeffs="imm", min_blocks=1),
+    "srt_sym_b128": dict(mode="sorted", block=128, radix=1, coeffs="imm", form="sym"),
+    "srt_imm_b256_pre32": dict(mode="sorted", block=256, radix=1, coeffs="imm", presort=32),
+    "srt_pre32": dict(mode="sorted", block=512, radix=1, coeffs="imm", presort=32),
+    "srt_pre64": dict(mode="sorted", block=512, radix=1, coeffs="imm", presort=64),
+    "srt_pre16": dict(mode="sorted", block=512, radix=1, coeffs="imm", presort=16),
+    "srt_sym_pre32": dict(mode="sorted", block=512, radix=1, coeffs="imm", form="sym", presort=32),
+    "l1_bin32_imm": dict(mode="binned", stage="l1", block=256, bin=32, coeffs="imm", branchy=True),
+    "l1_bin32_table": dict(mode="binned", stage="l1", block=256, bin=32, coeffs="table"),
 }
 
 
@@ -121,7 +146,7 @@ def main():
     grad = torch.empty((n, space.dim), device=dev)
     ref = None
     for name, over in VARIANTS.items():
-        if a.only and a.only not in name:
+        if a.only and name not in a.only.split(","):
             continue
         try:
             over = dict(over)
