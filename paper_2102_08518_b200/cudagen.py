@@ -75,6 +75,9 @@ class GenConfig:
     radix: int = 0               # 1: sub-region via a mixed-radix index of the plane-family counts
     rank: str = "match"          # sorted: rank in the psi class by "match" (warp-aggregated) | "atomic"
     presort: int = 0             # sorted: bin edge (cells) of a locality pre-sort of the queries (0 = off)
+    tpairs: int = 1              # sorted + table + tloop: 2 = two pairs of one polynomial per thread
+    cmajor: int = 0              # sorted: evaluate class by class (1; 2 = with a CTA barrier between
+                                 # classes) so the warps of an SM execute one polynomial's code
     tloop: int = 0               # coeffs="table": 1 = a runtime loop over the stencil sites (code
                                  # shared by every reference polynomial: no instruction-cache
                                  # pressure for large polynomials), 0 = fully unrolled
@@ -785,6 +788,8 @@ def generate(space, config: GenConfig | None = None, extents=None,
         if not t.uniform_tp:
             smem.append(("sg_tp", T, [float(v) for tp in t.tshift for v in tp]))
     fetch_mode = "uniform" if t.uniform_stencil else ("affine" if t.affine is not None else "table")
+    if cfg.tloop:
+        fetch_mode = "table"      # the site loop reads its offsets from the per-sub-region table
     if fetch_mode != "uniform" and not same_geom and not cfg.unroll_cosets:
         pass  # per-coset strides are compile-time constants in unrolled mode only; handled below
     if fetch_mode == "affine":
@@ -884,6 +889,13 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 static_b -= nb
             dyn_bytes = off - -(-pair_b // 16) * 16 + (-(-pair_b // 16) * 16 - pair_b)
 
+    if not sorted_:
+        elem = {"float": 4, "double": 8, "int": 4, "short": 2}
+        static_b = sum(elem[ct] * len(v) for _n, ct, v in smem)
+        if static_b > 46 * 1024:
+            raise ValueError(f"shared tables of {static_b} B exceed the 48 KB static limit "
+                             "(only mode='sorted' places large tables in dynamic shared memory)")
+
     # ---- kernel -------------------------------------------------------------
     def direct_preamble(pre="  "):
         """Per query (direct mode): the query point from xs[qi] + the fixed-point split."""
@@ -959,7 +971,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
         return out
 
     # sorted: 2 CTAs / SM by design; render: an explicit bound (ptxas otherwise caps at 48 regs)
-    min_blocks = cfg.min_blocks or ((1 if dyn_tables else 2) if sorted_
+    min_blocks = cfg.min_blocks or ((1 if (dyn_tables or cfg.tpairs == 2) else 2) if sorted_
                                     else (max(1, 256 // cfg.block) if (render or pack2) else 0))
     lb = f"{cfg.block}, {min_blocks}" if min_blocks else f"{cfg.block}"
     body = []
@@ -999,6 +1011,8 @@ def generate(space, config: GenConfig | None = None, extents=None,
             B("  __shared__ int sg_cnt[32];")
             B("  __shared__ int sg_start[32];")
             B("  __shared__ int sg_tot;")
+            if cfg.cmajor == 3:
+                B("  __shared__ int sg_next;")
             B("  if (threadIdx.x < 32) sg_cnt[threadIdx.x] = 0;")
             B("  const unsigned lane = threadIdx.x & 31u;")
             B("  const unsigned lt_mask = (1u << lane) - 1u;")
@@ -1737,6 +1751,8 @@ def generate(space, config: GenConfig | None = None, extents=None,
             w = 4 if T == "float" else 2
             comps = ["x", "y", "z", "w"][:w]
             L(f"const {vec}* __restrict__ Arow = reinterpret_cast<const {vec}*>(sg_A) + {psi_e};")
+            if sctx.get("dual"):
+                return run_table_dual(nmp, midx, psi_e, vec, w, comps)
             for m in range(nmp):
                 L(f"{T} g{m} = ({T})0;")
             u = None
@@ -1771,6 +1787,54 @@ def generate(space, config: GenConfig | None = None, extents=None,
                             L(f"{{ const {vec} a_ = Arow[{(j * tab['nq'] + q) * t.K}]; " + " ".join(
                                 f"g{q * w + r} = a_.{comps[r]} * c{j} + g{q * w + r};" for r in range(w)) + " }")
                     nchunk += 1
+            table_tail(nmp, midx, psi_e)
+
+        def run_table_dual(nmp, midx, psi_e, vec, w, comps):
+            """Sorted mode, two pairs A, B of one reference polynomial per thread: every
+            coefficient quad read from shared memory feeds 8 FMAs (4 per pair) -- the
+            single-pair loop is bound by the shared-memory pipe (one LDS.128 per 4 FMAs)."""
+            npad = t.n + 1 if t.n % 2 == 0 else t.n
+            L(f"const int* __restrict__ offA_ = &sg_off0[subA * {npad}];")
+            L(f"const int* __restrict__ offB_ = &sg_off0[subB * {npad}];")
+            for m in range(nmp):
+                L(f"{T} gA{m} = ({T})0, gB{m} = ({T})0;")
+            nsite = (f"sg_npsi[{psi_e}]" if not t.uniform_n else str(t.n))
+            L(f"const int ns_ = {nsite};")
+            L(f"{T} cnA_ = __ldg(V + (baseA + offA_[0])), cnB_ = __ldg(V + (baseB + offB_[0]));")
+            L("#pragma unroll 1")
+            L("for (int j_ = 0; j_ < ns_; ++j_) {")
+            L(f"  const {T} cjA_ = cnA_, cjB_ = cnB_;")
+            L("  if (j_ + 1 < ns_) { cnA_ = __ldg(V + (baseA + offA_[j_ + 1])); "
+              "cnB_ = __ldg(V + (baseB + offB_[j_ + 1])); }")
+            L(f"  const {vec}* __restrict__ Aj_ = Arow + j_ * {tab['nq'] * t.K};")
+            for q in range(nmp // w):
+                L(f"  {{ const {vec} a_ = Aj_[{q * t.K}]; " + " ".join(
+                    f"gA{q * w + r} = a_.{comps[r]} * cjA_ + gA{q * w + r}; "
+                    f"gB{q * w + r} = a_.{comps[r]} * cjB_ + gB{q * w + r};" for r in range(w)) + " }")
+            L("}")
+            for tag in "AB":
+                L("{")
+                em.indent += "  "
+                L(f"const int sub = sub{tag};")
+                for d in range(s):
+                    L(f"const {T} u{d} = u{tag}{d};")
+                for m in range(nmp):
+                    L(f"{T} g{m} = g{tag}{m};")
+                L(f"{T} acc = ({T})0;")
+                if cfg.grad:
+                    for d in range(s):
+                        L(f"{T} gacc{d} = ({T})0;")
+                table_tail(nmp, midx, psi_e)
+                if cfg.grad:
+                    gg = ", ".join([f"gacc{d}" for d in range(s)] + ["0.0f"] * (3 - s))
+                    L(f"sg_res4[pi{tag}] = make_float4(acc, {gg});")
+                else:
+                    L(f"sg_res[pi{tag}] = acc;")
+                em.indent = em.indent[:-2]
+                L("}")
+
+        def table_tail(nmp, midx, psi_e):
+            """acc (+ gacc) from the monomial coefficients g{m} in scope."""
             if tab["has_free"]:
                 L(f"const {T}* __restrict__ A0row = &sg_A0[{psi_e} * {nmp}];")
                 for m in range(tab["nm"]):
@@ -2079,6 +2143,8 @@ def generate(space, config: GenConfig | None = None, extents=None,
         body.append("      sg_start[lane] = v_ - c_;")
         body.append("      if (lane == 31) sg_tot = v_;")
         body.append("      sg_cnt[lane] = 0;")
+        if cfg.cmajor == 3:
+            body.append("      if (lane == 0) sg_next = 0;")
         body.append("    }")
         body.append("    __syncthreads();")
         psi_of = (lambda sub: str(t.psi[0])) if (t.K == 1 or t.uniform_psi) else (lambda sub: f"sg_psi[{sub}]")
@@ -2094,6 +2160,11 @@ def generate(space, config: GenConfig | None = None, extents=None,
         body.append("    const int tot = sg_tot;")
         pf = cfg.prefetch and fetch_mode in ("table", "uniform")
         sctx["prefetched"] = bool(pf)
+        dual = cfg.tpairs == 2
+        cmajor = bool(cfg.cmajor) and not dual and not pf and t.K > 1
+        if dual and not (cfg.coeffs == "table" and cfg.tloop and fetch_mode == "table"
+                         and not smem_fetch and same_geom):
+            raise ValueError("tpairs=2 needs coeffs='table', tloop=1 and per-sub-region offset tables")
         if pf:
             # software pipeline: pair pos + B's record, sub-region and coefficient gathers are
             # issued before pair pos's polynomial, so the gathers' latency hides behind it
@@ -2132,6 +2203,71 @@ def generate(space, config: GenConfig | None = None, extents=None,
             pf_load("        ", f"pos + {Bk}")
             body.append(f"      const float* __restrict__ V = (const float*)vol.base[0];")
             body.append("      const int base = 0;")
+        elif dual:
+            # two pairs per thread (adjacent in psi order: the same polynomial except at a
+            # class boundary, which takes the one-pair path below)
+            body.append(f"    for (int pos = 2 * (int)threadIdx.x; pos < tot; pos += {2 * Bk}) {{")
+            body.append("      const bool hasB = pos + 1 < tot;")
+            body.append("      const int eA = sg_ord[pos], eB = sg_ord[hasB ? pos + 1 : pos];")
+            body.append("      const int piA = eA & 0xffff, subA = eA >> 16, piB = eB & 0xffff, subB = eB >> 16;")
+            body.append(f"      const int psiA = {psi_of('subA')}, psiB = {psi_of('subB')};")
+            body.append(f"      const float* __restrict__ V = (const float*)vol.base[0];")
+            body.append("      if (hasB && psiA == psiB) {")
+            body.append("        const float4 rA = sg_rec[piA], rB = sg_rec[piB];")
+            for d in range(s):
+                body.append(f"        const float uA{d} = rA.{'xyz'[d]}, uB{d} = rB.{'xyz'[d]};")
+            body.append("        const int baseA = __float_as_int(rA.w), baseB = __float_as_int(rB.w);")
+            body.append("        const int psi = psiA;")
+            body.append("        const int sub = subA, base = baseA;")
+            em.lines = []
+            em.indent = "        "
+            sctx["dual"] = True
+            emit_coset(0, False, phase="eval")
+            sctx["dual"] = False
+            body.extend(em.lines)
+            body.append("      } else {")
+            body.append("      for (int h_ = 0; h_ < (hasB ? 2 : 1); ++h_) {")
+            body.append("      const int pi_ = h_ ? piB : piA;")
+            body.append("      const int sub = h_ ? subB : subA;")
+            body.append("      const float4 rec = sg_rec[pi_];")
+            for d in range(s):
+                body.append(f"      const float u{d} = rec.{'xyz'[d]};")
+            body.append("      const int base = __float_as_int(rec.w);")
+        elif cfg.cmajor == 3 and cmajor:
+            # warp-sized chunks of the psi-ordered pairs handed out in order (shared counter):
+            # the chunks in flight are a contiguous window of the order, i.e. at most two
+            # polynomials' code is live in the SM, with no barrier between polynomials
+            body.append("    for (;;) {")
+            body.append("      int ch_ = 0;")
+            body.append("      if (lane == 0) ch_ = atomicAdd(&sg_next, 1);")
+            body.append("      ch_ = __shfl_sync(0xffffffffu, ch_, 0);")
+            body.append("      if (ch_ * 32 >= tot) break;")
+            body.append("      const int pos = ch_ * 32 + (int)lane;")
+            body.append("      if (pos >= tot) continue;")
+            body.append("      const int e_ = sg_ord[pos];")
+            body.append("      const int pi_ = e_ & 0xffff;")
+            body.append("      const int sub = e_ >> 16;")
+            body.append("      const float4 rec = sg_rec[pi_];")
+            for d in range(s):
+                body.append(f"      const float u{d} = rec.{'xyz'[d]};")
+            body.append("      const int base = __float_as_int(rec.w);")
+            body.append(f"      const float* __restrict__ V = (const float*)vol.base[0];")
+        elif cmajor:
+            # class-major: one reference polynomial at a time for the whole CTA (its code
+            # stays in the SM's instruction cache); thread t keeps the positions p = t mod B
+            # of the unsorted loop, so the work per thread is unchanged
+            body.append(f"    for (int cls = 0; cls < {t.K}; ++cls) {{")
+            body.append("      const int c0 = sg_start[cls];")
+            body.append(f"      const int c1 = cls + 1 < {min(t.K, 32)} ? sg_start[cls + 1] : tot;")
+            body.append(f"      for (int pos = c0 + ((((int)threadIdx.x - c0) % {Bk}) + {Bk}) % {Bk}; pos < c1; pos += {Bk}) {{")
+            body.append("      const int e_ = sg_ord[pos];")
+            body.append("      const int pi_ = e_ & 0xffff;")
+            body.append("      const int sub = e_ >> 16;")
+            body.append("      const float4 rec = sg_rec[pi_];")
+            for d in range(s):
+                body.append(f"      const float u{d} = rec.{'xyz'[d]};")
+            body.append("      const int base = __float_as_int(rec.w);")
+            body.append(f"      const float* __restrict__ V = (const float*)vol.base[0];")
         else:
             body.append(f"    for (int pos = threadIdx.x; pos < tot; pos += {Bk}) {{")
             body.append("      const int e_ = sg_ord[pos];")
@@ -2143,7 +2279,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
             body.append("      const int base = __float_as_int(rec.w);")
             body.append(f"      const float* __restrict__ V = (const float*)vol.base[0];")
         if t.K > 1:
-            body.append(f"      const int psi = {psi_of('sub')};")
+            body.append(f"      const int psi = {'cls' if (cmajor and cfg.cmajor != 3) else psi_of('sub')};")
         body.append("      float acc = 0.0f;")
         if cfg.grad:
             for d in range(s):
@@ -2157,6 +2293,13 @@ def generate(space, config: GenConfig | None = None, extents=None,
             body.append(f"      sg_res4[pi_] = make_float4(acc, {g});")
         else:
             body.append("      sg_res[pi_] = acc;")
+        if dual:
+            body.append("      }")   # one-pair loop
+            body.append("      }")   # one-pair path
+        if cmajor and cfg.cmajor != 3:
+            body.append("      }")   # positions of this class
+            if cfg.cmajor == 2:
+                body.append("      __syncthreads();")
         body.append("    }")
         body.append("    __syncthreads();")
         if render:

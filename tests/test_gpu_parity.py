@@ -31,7 +31,12 @@ def _evaluator(space, arrays, **kw):
         pytest.skip("pack=2 needs one stencil size for every sub-region")
     dt = np.float32 if fw == "f32" else np.float64
     cfg = GenConfig(params=params, float_width=fw, **kw)
-    return Evaluator(space, [a.astype(dt) for a in arrays], cfg)
+    try:
+        return Evaluator(space, [a.astype(dt) for a in arrays], cfg)
+    except ValueError as e:
+        if "48 KB static limit" in str(e):
+            pytest.skip(str(e))
+        raise
 
 
 def _xs(z, which, dtype=torch.float32):
@@ -98,6 +103,9 @@ CONFIGS = [
     dict(mode="sorted", form="sym", block=256, tile=512),
     dict(mode="sorted", coeffs="table", tile=256),
     dict(mode="sorted", params_md=(2, 4), form="sites"),
+    dict(mode="sorted", coeffs="table", tloop=1),
+    dict(mode="sorted", coeffs="table", tloop=1, tpairs=2, block=256, radix=1),
+    dict(coeffs="table", tloop=1),
 ]
 
 
@@ -139,7 +147,7 @@ def test_values_f64_variant(name):
 
 @pytest.mark.parametrize("name", golden_names())
 @pytest.mark.parametrize("mode", ["direct", "binned", "table", "sym", "sorted", "sorted_sym",
-                                  "pack2", "pack2_binned_sym", "presort"])
+                                  "pack2", "pack2_binned_sym", "presort", "sorted_table_pairs"])
 def test_gradient_vs_oracle(name, mode):
     space, ospace, z, arrays = load_golden(name)
     xs = z["uniform_xs"].astype(np.float64)
@@ -155,6 +163,9 @@ def test_gradient_vs_oracle(name, mode):
         ev = _evaluator(space, arrays, grad=True, pack=2)
     elif mode == "presort":
         ev = _evaluator(space, arrays, grad=True, mode="sorted", presort=4)
+    elif mode == "sorted_table_pairs":
+        ev = _evaluator(space, arrays, grad=True, mode="sorted", coeffs="table", tloop=1, tpairs=2,
+                        block=256)
     elif mode == "pack2_binned_sym":
         ev = _evaluator(space, arrays, grad=True, pack=2, mode="binned", form="sym")
     else:

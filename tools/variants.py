@@ -115,6 +115,37 @@ VARIANTS = {
     "tl384": dict(mode="sorted", block=384, radix=1, coeffs="table", tloop=1),
     "tl512_t1024": dict(mode="sorted", block=512, tile=1024, radix=1, coeffs="table", tloop=1),
     "tl256_t1024": dict(mode="sorted", block=256, tile=1024, radix=1, coeffs="table", tloop=1),
+    "tp2_256": dict(mode="sorted", block=256, radix=1, coeffs="table", tloop=1, tpairs=2),
+    "tp2_256_t1024": dict(mode="sorted", block=256, tile=1024, radix=1, coeffs="table", tloop=1, tpairs=2),
+    "tp2_256_t2048": dict(mode="sorted", block=256, tile=2048, radix=1, coeffs="table", tloop=1, tpairs=2),
+    "tp2_128": dict(mode="sorted", block=128, radix=1, coeffs="table", tloop=1, tpairs=2),
+    "tp2_256_pre32": dict(mode="sorted", block=256, radix=1, coeffs="table", tloop=1, tpairs=2, presort=32),
+    "cm1_b384": dict(mode="sorted", block=384, radix=1, coeffs="imm", min_blocks=1, cmajor=1),
+    "cm2_b384": dict(mode="sorted", block=384, radix=1, coeffs="imm", min_blocks=1, cmajor=2),
+    "cm1_b384_t3072": dict(mode="sorted", block=384, tile=3072, radix=1, coeffs="imm", min_blocks=1, cmajor=1),
+    "cm2_b384_t3072": dict(mode="sorted", block=384, tile=3072, radix=1, coeffs="imm", min_blocks=1, cmajor=2),
+    "cm2_b384_t4608": dict(mode="sorted", block=384, tile=4608, radix=1, coeffs="imm", min_blocks=1, cmajor=2),
+    "cm1_b512_t4096": dict(mode="sorted", block=512, tile=4096, radix=1, coeffs="imm", min_blocks=1, cmajor=1),
+    "cm2_b512_t4096": dict(mode="sorted", block=512, tile=4096, radix=1, coeffs="imm", min_blocks=1, cmajor=2),
+    "cm1_b256_t2048": dict(mode="sorted", block=256, tile=2048, radix=1, coeffs="imm", cmajor=1),
+    "cm1_tl512": dict(mode="sorted", block=512, radix=1, coeffs="table", tloop=1, cmajor=1),
+    "cm3_b384": dict(mode="sorted", block=384, radix=1, coeffs="imm", min_blocks=1, cmajor=3),
+    "cm3_b384_t3072": dict(mode="sorted", block=384, tile=3072, radix=1, coeffs="imm", min_blocks=1, cmajor=3),
+    "cm2_b384_t3840": dict(mode="sorted", block=384, tile=3840, radix=1, coeffs="imm", min_blocks=1, cmajor=2),
+    "cm3_b384_t3840": dict(mode="sorted", block=384, tile=3840, radix=1, coeffs="imm", min_blocks=1, cmajor=3),
+    "cm3_b256_t2048": dict(mode="sorted", block=256, tile=2048, radix=1, coeffs="imm", cmajor=3),
+    "cm3_b256_t3072": dict(mode="sorted", block=256, tile=3072, radix=1, coeffs="imm", min_blocks=1, cmajor=3),
+    "cm3_b512_t3072": dict(mode="sorted", block=512, tile=3072, radix=1, coeffs="imm", min_blocks=1, cmajor=3),
+    "cm3_sym_b384_t3072": dict(mode="sorted", block=384, tile=3072, radix=1, coeffs="imm", min_blocks=1, cmajor=3, form="sym"),
+    "cm3_b512_t2048": dict(mode="sorted", block=512, tile=2048, radix=1, coeffs="imm", min_blocks=1, cmajor=3),
+    "cm3_b512_t2560": dict(mode="sorted", block=512, tile=2560, radix=1, coeffs="imm", min_blocks=1, cmajor=3),
+    "cm3_b512_t3584": dict(mode="sorted", block=512, tile=3584, radix=1, coeffs="imm", min_blocks=1, cmajor=3),
+    "cm3_b640_t3200": dict(mode="sorted", block=640, tile=3200, radix=1, coeffs="imm", min_blocks=1, cmajor=3),
+    "cm3_b768_t3072": dict(mode="sorted", block=768, tile=3072, radix=1, coeffs="imm", min_blocks=1, cmajor=3),
+    "cm3_b1024_t3072": dict(mode="sorted", block=1024, tile=3072, radix=1, coeffs="imm", min_blocks=1, cmajor=3),
+    "cm3_b512_t1536_g": dict(mode="sorted", block=512, tile=1536, radix=1, coeffs="imm", min_blocks=1, cmajor=3),
+    "cm3_sym_b512_t1536": dict(mode="sorted", block=512, tile=1536, radix=1, coeffs="imm", min_blocks=1, cmajor=3, form="sym"),
+    "cm3_b256_t1024_mb2": dict(mode="sorted", block=256, tile=1024, radix=1, coeffs="imm", min_blocks=2, cmajor=3),
     "srt_imm_b128": dict(mode="sorted", block=128, radix=1, coeffs="imm"),
     "srt_imm_b256_t512": dict(mode="sorted", block=256, tile=512, radix=1, coeffs="imm"),
     "srt_imm_b256_t2048": dict(mode="sorted", block=256, tile=2048, radix=1, coeffs="imm"),
