@@ -49,42 +49,50 @@ CONFIGS = {
                grad=False, scaling="weak",
                variant=dict(mode="binned", coeffs="imm", form="sym", block=512),
                desc="BCC quintic box spline (4 dirs x2), 2x101^3 coset-split, 2^24 uniform"),
-    "c3": dict(space="bcc_voronoi2", extents=(203, 203, 203), queries=1 << 26, kind="rays",
+    "c3": dict(space="bcc_voronoi3", extents=(203, 203, 203), queries=1 << 26, kind="rays",
                rays=(512, 512, 256), grad=False, scaling="weak",
-               variant=dict(mode="sorted", coeffs="imm", block=512, radix=1),
-               desc="BCC Voronoi spline (order 2, piecewise cubic), 2x203^3, 2^26 ray-ordered"),
+               variant=dict(mode="sorted", coeffs="imm", block=640, tile=3200, radix=1, min_blocks=1,
+                            cmajor=3),
+               desc="BCC Voronoi spline (order 3: the paper's BCC Voronoi case, 14 reference "
+                    "polynomials), 2x203^3, 2^26 ray-ordered"),
+    "c3o2": dict(space="bcc_voronoi2", extents=(203, 203, 203), queries=1 << 26, kind="rays",
+                 rays=(512, 512, 256), grad=False, scaling="weak",
+                 variant=dict(mode="sorted", coeffs="imm", block=512, radix=1),
+                 desc="BCC Voronoi spline (order 2, piecewise cubic), 2x203^3, 2^26 ray-ordered"),
     "c4": dict(space="fcc_box6", extents=(161, 161, 161), queries=1 << 26, kind="uniform",
                grad=True, scaling="weak", variant=dict(mode="direct", coeffs="imm", block=128),
                desc="FCC 6-direction box spline, 4x161^3, 2^26 uniform, value + gradient"),
-    "c4v": dict(space="fcc_voronoi2", extents=(161, 161, 161), queries=1 << 26, kind="uniform",
+    "c4vo2": dict(space="fcc_voronoi2", extents=(161, 161, 161), queries=1 << 26, kind="uniform",
                 grad=True, scaling="weak", variant=dict(mode="direct", coeffs="table", block=128),
                 desc="FCC Voronoi spline (order 2), 4x161^3, 2^26 uniform, value + gradient"),
-    "c4v3": dict(space="fcc_voronoi3", extents=(161, 161, 161), queries=1 << 26, kind="uniform",
-                 grad=True, scaling="weak", variant=dict(mode="sorted", coeffs="imm", block=512, radix=1),
+    "c4v": dict(space="fcc_voronoi3", extents=(161, 161, 161), queries=1 << 26, kind="uniform",
+                 grad=True, scaling="weak",
+                 variant=dict(mode="sorted", coeffs="imm", form="sym", block=512, radix=1, presort=32),
                  desc="FCC Voronoi spline (order 3, the paper's FCC case), 4x161^3, 2^26 uniform, "
                       "value + gradient"),
-    "c3v3": dict(space="bcc_voronoi3", extents=(203, 203, 203), queries=1 << 26, kind="rays",
-                 rays=(512, 512, 256), grad=False, scaling="weak",
-                 variant=dict(mode="sorted", coeffs="imm", block=512, radix=1),
-                 desc="BCC Voronoi spline (order 3, the paper's K=7 case), 2x203^3, 2^26 ray-ordered"),
-    "c5u": dict(space="bcc_voronoi2", extents=(406, 406, 406), queries=1 << 30, kind="uniform",
+    "c5u": dict(space="bcc_voronoi3", extents=(406, 406, 406), queries=1 << 30, kind="uniform",
                 grad=False, scaling="strong",
                 variant=dict(mode="binned", stage="l1", block=256, bin=136, coeffs="imm"),
                 desc="c5 with uniform random queries (SURVEY 8d secondary): 535 MB volume > L2; "
                      "a coarse locality sort (136-cell bins, no bricks) keeps the gathers in L2"),
-    "c3r": dict(space="bcc_voronoi2", extents=(203, 203, 203), queries=1 << 26, kind="render",
+    "c3r": dict(space="bcc_voronoi3", extents=(203, 203, 203), queries=1 << 26, kind="render",
                 rays=(512, 512, 256), grad=False, scaling="weak", variant=dict(),
                 desc="fused volume render of c3: 512x512 rays x 256 samples through 2x203^3 BCC "
                      "Voronoi (ray march + psi-sorted reconstruction + compositing in one kernel)"),
-    "c3rs": dict(space="bcc_voronoi2", extents=(203, 203, 203), queries=1 << 26, kind="render",
+    "c3rs": dict(space="bcc_voronoi3", extents=(203, 203, 203), queries=1 << 26, kind="render",
                  rays=(512, 512, 256), grad=True, scaling="weak", variant=dict(),
                  desc="c3r with gradient (Lambert) shading at every sample"),
-    "c5": dict(space="bcc_voronoi2", extents=(406, 406, 406), queries=1 << 30, kind="rays",
-               rays=(1024, 1024, 1024), grad=False, scaling="strong",
-               variant=dict(mode="sorted", coeffs="imm", block=512, radix=1),
-               desc="BCC Voronoi spline (order 2), 2x406^3, 2^30 ray-ordered sharded over the GPUs"),
+    "c5": dict(space="bcc_voronoi3", extents=(406, 406, 406), queries=1 << 30, kind="rays",
+               rays=(1024, 1024, 1024), grad=False, scaling="strong", steps=20,
+               variant=dict(mode="sorted", coeffs="imm", block=640, tile=3200, radix=1, min_blocks=1,
+                            cmajor=3),
+               desc="BCC Voronoi spline (order 3), 2x406^3, 2^30 ray-ordered sharded over the GPUs"),
+    "c5o2": dict(space="bcc_voronoi2", extents=(406, 406, 406), queries=1 << 30, kind="rays",
+                 rays=(1024, 1024, 1024), grad=False, scaling="strong", steps=20,
+                 variant=dict(mode="sorted", coeffs="imm", block=512, radix=1),
+                 desc="BCC Voronoi spline (order 2), 2x406^3, 2^30 ray-ordered sharded over the GPUs"),
 }
-DEFAULT_CONFIG = "c2"
+DEFAULT_CONFIG = "c5"
 
 
 def _space_available(name):
@@ -342,7 +350,7 @@ def cpu_model():
     return None
 
 
-def roofline(cfg_name, falg, n, eval_kernel_ms, step_ms, pk):
+def roofline(cfg_name, falg, n, eval_kernel_ms, step_ms, pk, kernel_key=None):
     """roofline block of the bench line for the dominant kernel (sg_eval_kernel).
 
     achieved = algorithmic FP32 work (the reference's own dynamic op count F_alg per query,
@@ -389,8 +397,11 @@ def roofline(cfg_name, falg, n, eval_kernel_ms, step_ms, pk):
                     f"({pk['source']} sm_max_mhz); binding roof = max(F_alg / FP32 peak, "
                     f"B_alg / HBM) per query (SURVEY 8d)"})
     prof = PROFILES / f"ncu_{cfg_name}.json"
-    if prof.exists():
-        d = json.loads(prof.read_text())
+    d = json.loads(prof.read_text()) if prof.exists() else None
+    if d is not None and d.get("kernel_key") != kernel_key:
+        roof["profile"] = f"{prof.name} is from another kernel variant (stale): not used"
+        d = None
+    if d is not None:
         roof["traffic"] = d.get("dram_bytes_per_launch")
         ex = d.get("executed_fp32_flops_per_query")
         if ex:
@@ -542,7 +553,7 @@ def run_ours(args, rank, world, device):
         return None
     pk = peaks()
     falg = falg_per_query(c["space"])
-    roof = roofline(args.config, falg, n, eval_kernel_ms, kernel_ms, pk)
+    roof = roofline(args.config, falg, n, eval_kernel_ms, kernel_ms, pk, prog.key)
     line = {
         "metric": "G reconstructions/sec per B200 (fraction of FP32 roofline in roofline)",
         "value": round(value, 4), "unit": "Grecon/s", "n_gpus": world, "steps": args.steps,
@@ -631,7 +642,7 @@ def run_render(args, rank, world, device):
         return None
     pk = peaks()
     falg = falg_per_query(c["space"])
-    roof = roofline(args.config, falg, n, step_ms, step_ms, pk)
+    roof = roofline(args.config, falg, n, step_ms, step_ms, pk, r.prog.key)
     line = {
         "metric": "G reconstructions/sec per B200 (fraction of FP32 roofline in roofline)",
         "value": round(value, 4), "unit": "Grecon/s", "n_gpus": world, "steps": args.steps,
@@ -749,7 +760,8 @@ def _cpu_worker_init(cfg_name, arrays, xs, shard):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: the configuration's, 300 or 20 for c5)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default=None)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
@@ -760,6 +772,8 @@ def main():
                          "NCCL/NVLink, SURVEY 8e), reported separately as gather_ms")
     args = ap.parse_args()
     args.config = args.config or default_config_name()
+    if args.steps is None:
+        args.steps = CONFIGS[args.config].get("steps", 300)
     args.warmup = max(3, args.warmup)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -42,7 +42,18 @@ def render_config(space: SplineSpace, shade: bool = False, **variant) -> GenConf
     kw = dict(params=ScheduleParams(1, space.stencil_size, "predicated"), mode="render",
               grad=shade, block=128)
     if len(space.ref_polys) > 1:
-        kw.update(block=256, tile=1024) if shade else kw.update(block=512, tile=1536)
+        big = sum(len(rp.poly.terms) for rp in space.ref_polys) > 4000
+        if big and shade:
+            # value + gradient of large polynomials: coefficient tables in shared memory and
+            # one site loop for all of them (the gradient comes from the same monomial sums);
+            # per-polynomial immediate code (x4 with the derivatives) overflows the I-cache
+            kw.update(block=384, tile=768, coeffs="table", tloop=1)
+        elif big:
+            # immediates, warp chunks handed out in polynomial order (cmajor=3): measured on
+            # B200 for the order-3 BCC Voronoi spline, 45.0 -> 10.5 ms per 512 x 512 x 256
+            kw.update(block=512, tile=3072, cmajor=3, min_blocks=1)
+        else:
+            kw.update(block=256, tile=1024) if shade else kw.update(block=512, tile=1536)
         kw.update(radix=1)   # sub-region from the plane-family counts when they cover every plane
     kw.update(variant)
     return GenConfig(**kw)

@@ -22,6 +22,17 @@ def num(rec, k):
         return 0.0
 
 
+def kernel_key(cfg):
+    """Source hash of the configuration's kernel (bench.py ignores a stale profile)."""
+    c = bench.CONFIGS[cfg]
+    if c["kind"] == "render":
+        from paper_2102_08518_b200 import generate, load_fixture
+        from paper_2102_08518_b200.render import render_config
+        sp = load_fixture(c["space"])
+        return generate(sp, render_config(sp, c["grad"], **c.get("variant", {})), c["extents"]).key
+    return bench.build_program(cfg)[1].key
+
+
 def main():
     cfg, rep = sys.argv[1], sys.argv[2]
     tag = sys.argv[3] if len(sys.argv) > 3 else "r01"
@@ -57,6 +68,7 @@ def main():
         "l2_hit_pct": num(rec, "lts__t_sector_hit_rate.pct"),
         "warps_active_pct": num(rec, "sm__warps_active.avg.pct_of_peak_sustained_active"),
         "registers": num(rec, "launch__registers_per_thread"),
+        "kernel_key": kernel_key(cfg),
     }
     p = ROOT / "profiles" / f"ncu_{cfg}.json"
     p.write_text(json.dumps(out, indent=1) + "\n")

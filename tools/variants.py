@@ -22,6 +22,17 @@ from paper_2102_08518_b200 import runtime  # noqa: E402
 
 RENDER_VARIANTS = {
     "march": dict(),
+    "r_tl_b512_t1536": dict(block=512, tile=1536, radix=1, coeffs="table", tloop=1),
+    "r_tl_b512_t1024": dict(block=512, tile=1024, radix=1, coeffs="table", tloop=1),
+    "r_tl_cm3_b512_t1536": dict(block=512, tile=1536, radix=1, coeffs="table", tloop=1, cmajor=3),
+    "r_tl_b384_t768": dict(block=384, tile=768, radix=1, coeffs="table", tloop=1),
+    "r_tl_cm3_b512_t1024": dict(block=512, tile=1024, radix=1, coeffs="table", tloop=1, cmajor=3),
+    "r_tl_b256_t1024": dict(block=256, tile=1024, radix=1, coeffs="table", tloop=1),
+    "r_cm3_b640_t3200": dict(block=640, tile=3200, radix=1, cmajor=3, min_blocks=1),
+    "r_cm3_b512_t3072": dict(block=512, tile=3072, radix=1, cmajor=3, min_blocks=1),
+    "r_cm3_b512_t2048": dict(block=512, tile=2048, radix=1, cmajor=3, min_blocks=1),
+    "r_cm3_b256_t1536": dict(block=256, tile=1536, radix=1, cmajor=3, min_blocks=1),
+    "r_cm3_b384_t2304": dict(block=384, tile=2304, radix=1, cmajor=3, min_blocks=1),
     "sorted_b256_t1536": dict(block=256, tile=1536),
     "sorted_b256_t1024": dict(block=256, tile=1024),
     "sorted_b512_t1536": dict(block=512, tile=1536),
@@ -219,7 +230,7 @@ def render_variants(a, c):
     w, h, steps = c["rays"]
     ref = None
     for name, over in RENDER_VARIANTS.items():
-        if a.only and a.only not in name:
+        if a.only and name not in a.only.split(","):
             continue
         try:
             r = Renderer(space, arrays, w, h, steps, shade=c["grad"], **over)
