@@ -35,6 +35,8 @@ from pathlib import Path
 import numpy as np
 
 HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE.parents[1]))
+from tests.adversarial import adversarial_points  # noqa: E402  (the generator, shared with the GPU tests)
 REF_SRC = Path(os.environ.get("SPLINEGEN_REF", "/root/reference/pkg/src"))
 sys.dont_write_bytecode = True
 sys.path.insert(0, str(REF_SRC))
@@ -60,45 +62,6 @@ FP_OPS = ("fadd", "fsub", "fmul", "fneg", "fdiv")
 
 def _f32(a):
     return np.asarray(a, dtype=np.float32).astype(np.float64)
-
-
-def adversarial_points(space, extents, rng, count):
-    """Inputs that expose fp32 selection bugs: k+1/2 +- 1 ulp(f32),
-    tiny |x| next to coset offsets, points exactly on BSP planes (>= decides),
-    and points outside [0, E) (periodic wrap)."""
-    s = space.dim
-    e = np.array(extents, dtype=np.float64)
-    pts = []
-    per = max(1, count // 5)
-    # 1) k + 1/2 (+-1 ulp f32) on random axes
-    base = np.floor(rng.random((per, s)) * e) + 0.5
-    for sign in (-1, 0, 1):
-        p = base.astype(np.float32)
-        if sign:
-            p = np.nextafter(p, np.float32(sign * np.inf))
-        pts.append(p.astype(np.float64))
-    # 2) tiny coordinates next to coset offsets
-    tiny = (rng.random((per, s)) - 0.5) * 2e-9
-    for off in space.lattice.cosets:
-        o = np.array([float(q) for q in off])
-        pts.append(_f32(o + tiny + np.floor(rng.random((per, s)) * 2)))
-    # 3) exactly on BSP planes, at dyadic positions near lattice sites
-    if space.planes:
-        for plane in space.planes:
-            nrm = np.array([float(v) for v in plane.normal])
-            site = np.floor(rng.random((per, s)) * e)
-            loc = np.round((rng.random((per, s)) - 0.5) * 64) / 64
-            # project loc onto the plane normal . loc = offset along the largest axis
-            ax = int(np.argmax(np.abs(nrm)))
-            rest = loc @ nrm - nrm[ax] * loc[:, ax]
-            loc[:, ax] = (float(plane.offset) - rest) / nrm[ax]
-            cand = site + loc
-            ok = np.all(np.abs(cand - np.round(cand * 64) / 64) == 0, axis=1)
-            pts.append(cand[ok])
-    # 4) out-of-range (negative and beyond the extent)
-    pts.append(_f32((rng.random((per, s)) - 0.5) * 4 * e))
-    out = np.concatenate(pts, axis=0)
-    return _f32(out)
 
 
 def grid_points(space, extents, rng, count):

@@ -99,3 +99,58 @@ def test_multi_rank_bench_code_path():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["parallelism"].startswith("query shards x2")
     assert d["gather_ms"] is not None and d["gather_ms"] > 0
+
+
+SELECT_CFGS = ["c1", "c2", "c3", "c4", "c4v", "c5", "c5u", "c3o2"]
+
+
+@pytest.mark.parametrize("cfg", SELECT_CFGS)
+def test_selection_bit_exact_full_size(cfg):
+    """The exact bench kernel variant with dbg=True at the configuration's full extents:
+    lattice shift k and sub-region of every (query, coset) bit-exact against the oracle on
+    >= 64K adversarial queries scaled to those extents (k + 1/2 +- ulp, |x| < 1e-9 at coset
+    offsets, on-plane points, out-of-range) plus bin-edge / wrap-border points and a slice
+    of the configuration's own query stream; values against the oracle on a subset."""
+    from tests.adversarial import adversarial_points, border_points
+    c = bench.CONFIGS[cfg]
+    dev = torch.device("cuda", 0)
+    space, arrays, _ = bench.make_inputs(cfg, 0, dev)
+    _, prog = bench.build_program(cfg, dbg=True)
+    ev = Evaluator(space, arrays, prog=prog)
+    rng = np.random.default_rng(31)
+    ext = c["extents"]
+    sets = [adversarial_points(space, ext, rng, 1 << 16),
+            border_points(ext, prog.bin or prog.presort, rng, 1 << 14),
+            bench.make_queries(cfg, 0, 1 << 14, dev).double().cpu().numpy()]
+    xs = np.concatenate(sets).astype(np.float32)
+    assert len(xs) >= 1 << 16
+    osp = refeval.load_space_file(SPACES_DIR / f"{space.name}.json")
+    # the fp64 oracle itself raises UnreachableRegionError on a few of these (e.g. a
+    # denormal coordinate next to a plane vertex: the rounded dot products give a sign
+    # vector no region has, oracle.py:56-74); the kernel must flag exactly those
+    x64 = xs.astype(np.float64)
+    bad = np.zeros(len(xs), dtype=bool)
+    for off in osp.cosets:
+        _, xloc = refeval.rho(osp, x64 - np.array([float(q) for q in off]))
+        if osp.planes:
+            bad |= np.array(osp.sigma, dtype=np.int64)[refeval.plane_q(osp, xloc)] < 0
+    if bad.any():
+        from paper_2102_08518_b200 import UnreachableRegionError
+        with pytest.raises(UnreachableRegionError):
+            ev(torch.from_numpy(xs[bad][:1]).cuda())
+        xs = xs[~bad]
+    r = ev(torch.from_numpy(xs).cuda())
+    out, dbg = r[0], r[2]
+    dbg = dbg.cpu().numpy()
+    x64 = xs.astype(np.float64)
+    s = space.dim
+    for ci, (k, sub) in enumerate(refeval.selection(osp, x64)):
+        bad = np.flatnonzero((dbg[:, ci, :s] != k).any(axis=1) | (dbg[:, ci, s] != sub))
+        assert bad.size == 0, (cfg, ci, bad[:5], x64[bad[:5]])
+    pick = rng.choice(len(xs), size=3000, replace=False)
+    grad = prog.has_grad
+    ref = refeval.reference_eval_batch(osp, x64[pick], [a.astype(np.float64) for a in arrays],
+                                       grad=grad)
+    want = ref[0] if grad else ref
+    got = out.double().cpu().numpy()[pick]
+    assert np.all(np.abs(got - want) <= 1e-6 + 1e-5 * np.maximum(np.abs(got), np.abs(want)))

@@ -157,6 +157,27 @@ VARIANTS = {
     "cm3_b512_t1536_g": dict(mode="sorted", block=512, tile=1536, radix=1, coeffs="imm", min_blocks=1, cmajor=3),
     "cm3_sym_b512_t1536": dict(mode="sorted", block=512, tile=1536, radix=1, coeffs="imm", min_blocks=1, cmajor=3, form="sym"),
     "cm3_b256_t1024_mb2": dict(mode="sorted", block=256, tile=1024, radix=1, coeffs="imm", min_blocks=2, cmajor=3),
+    "tl256_pre32": dict(mode="sorted", block=256, radix=1, coeffs="table", tloop=1, presort=32),
+    "tl512_pre32": dict(mode="sorted", block=512, radix=1, coeffs="table", tloop=1, presort=32),
+    "tl384_pre32_mb1": dict(mode="sorted", block=384, radix=1, coeffs="table", tloop=1, presort=32, min_blocks=1),
+    "srt_sym_pre16": dict(mode="sorted", block=512, radix=1, coeffs="imm", form="sym", presort=16),
+    "srt_sym_pre64": dict(mode="sorted", block=512, radix=1, coeffs="imm", form="sym", presort=64),
+    "srt_sym_pre32_b256": dict(mode="sorted", block=256, radix=1, coeffs="imm", form="sym", presort=32),
+    "srt_sym_pre32_mb1": dict(mode="sorted", block=512, radix=1, coeffs="imm", form="sym", presort=32, min_blocks=1),
+    "direct_pre": dict(mode="sorted", block=256, coeffs="imm", presort=32),
+    "l1_bin24": dict(mode="binned", stage="l1", block=256, bin=24),
+    "l1_bin16": dict(mode="binned", stage="l1", block=256, bin=16),
+    "l1_bin40": dict(mode="binned", stage="l1", block=256, bin=40),
+    "l1_bin16_b128": dict(mode="binned", stage="l1", block=128, bin=16),
+    "cm3_sym_pre32": dict(mode="sorted", block=512, radix=1, coeffs="imm", form="sym", presort=32, cmajor=3),
+    "cm3_sym_pre32_mb1_t2048": dict(mode="sorted", block=512, tile=2048, radix=1, coeffs="imm", form="sym", presort=32, cmajor=3, min_blocks=1),
+    "cm3_imm_pre32": dict(mode="sorted", block=512, radix=1, coeffs="imm", presort=32, cmajor=3),
+    "c4_branchy": dict(mode="direct", block=128, coeffs="imm", branchy=True),
+    "c4_sym": dict(mode="direct", block=128, coeffs="imm", form="sym"),
+    "c4_srt": dict(mode="sorted", block=256, coeffs="imm"),
+    "c4_srt_sym_b512": dict(mode="sorted", block=512, coeffs="imm", form="sym"),
+    "c4_direct_b256": dict(mode="direct", block=256, coeffs="imm"),
+    "c4_direct_f64sel": dict(mode="direct", block=128, coeffs="imm", radix=1),
     "srt_imm_b128": dict(mode="sorted", block=128, radix=1, coeffs="imm"),
     "srt_imm_b256_t512": dict(mode="sorted", block=256, tile=512, radix=1, coeffs="imm"),
     "srt_imm_b256_t2048": dict(mode="sorted", block=256, tile=2048, radix=1, coeffs="imm"),
