@@ -70,6 +70,11 @@ CONFIGS = {
                  variant=dict(mode="sorted", coeffs="imm", form="sym", block=512, radix=1, presort=32),
                  desc="FCC Voronoi spline (order 3, the paper's FCC case), 4x161^3, 2^26 uniform, "
                       "value + gradient"),
+    "c4v4": dict(space="fcc_voronoi4", extents=(161, 161, 161), queries=1 << 26, kind="uniform",
+                 grad=True, scaling="weak",
+                 variant=dict(mode="sorted", coeffs="table", tloop=1, tchunk=112, block=256, radix=1,
+                              presort=32),
+                 desc="FCC Voronoi spline (order 4, 'cubic'), 4x161^3, 2^26 uniform, value + gradient"),
     "c5u": dict(space="bcc_voronoi3", extents=(406, 406, 406), queries=1 << 30, kind="uniform",
                 grad=False, scaling="strong",
                 variant=dict(mode="binned", stage="l1", block=256, bin=136, coeffs="imm"),
@@ -141,11 +146,13 @@ def precompile_bench_kernels():
         compile_source(prog.source)
 
 
-def falg_per_query(space_name):
-    """Reference dynamic FP-op count (m=1, d=n, branchy), pinned by the golden script."""
+def falg_per_query(space_name, grad=False):
+    """Reference dynamic FP-op count (m=1, d=n, branchy), pinned by the golden script; with
+    `grad`, plus the gradient's ops by the same counting rule applied to the reference's
+    derivative polynomials (tests/golden/make_golden.py: falg_gradient_extra)."""
     p = ROOT / "tests" / "golden" / "falg.json"
     d = json.loads(p.read_text()) if p.exists() else {}
-    return d.get(space_name)
+    return d.get(space_name + "+grad" if grad else space_name)
 
 
 def peaks():
@@ -379,6 +386,11 @@ def roofline(cfg_name, falg, n, eval_kernel_ms, step_ms, pk, kernel_key=None):
                      "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(a / pk["hbm_gbs"], 4),
                      "volume_bytes": vol_bytes}
     achieved = falg * n / (eval_kernel_ms / 1e3) / 1e12
+    if c["grad"]:
+        f0 = falg_per_query(c["space"])
+        a0 = f0 * n / (eval_kernel_ms / 1e3) / 1e12
+        value_only = {"falg": f0, "achieved": round(a0, 3), "frac": round(a0 / pk["fp32_tflops"], 4),
+                      "unit": "TFLOP/s", "note": "value-only F_alg (the reference evaluates no gradient)"}
     if hbm_block and t_hbm > t_fp:
         roof = {"bound": "hbm", "achieved": hbm_block["achieved"], "peak": pk["hbm_gbs"],
                 "unit": "GB/s", "frac": hbm_block["frac"], "traffic": None,
@@ -389,9 +401,12 @@ def roofline(cfg_name, falg, n, eval_kernel_ms, step_ms, pk, kernel_key=None):
                 "unit": "TFLOP/s", "frac": round(achieved / pk["fp32_tflops"], 4), "traffic": None}
         if hbm_block:
             roof["hbm"] = hbm_block
+    if c["grad"]:
+        roof["value_only"] = value_only
     roof.update({
-            "note": f"F_alg = {falg:g} FP ops/query (reference dynamic count, m=1 d=n branchy; "
-                    f"tests/golden/falg.json) x {n} queries / sg_eval_kernel time "
+            "note": f"F_alg = {falg:g} FP ops/query (reference dynamic count, m=1 d=n branchy"
+                    + ("; value + gradient: the same counting rule on the derivative polynomials"
+                       if c["grad"] else "") + f"; tests/golden/falg.json) x {n} queries / sg_eval_kernel time "
                     f"({eval_kernel_ms:.4f} ms of the {step_ms:.4f} ms step, CUDA events on the "
                     f"launch stream); peak = 148 SM x 128 FP32 lanes x 2 x {pk['sm_max_mhz']:.0f} MHz "
                     f"({pk['source']} sm_max_mhz); binding roof = max(F_alg / FP32 peak, "
@@ -552,7 +567,7 @@ def run_ours(args, rank, world, device):
     if rank != 0:
         return None
     pk = peaks()
-    falg = falg_per_query(c["space"])
+    falg = falg_per_query(c["space"], c["grad"])
     roof = roofline(args.config, falg, n, eval_kernel_ms, kernel_ms, pk, prog.key)
     line = {
         "metric": "G reconstructions/sec per B200 (fraction of FP32 roofline in roofline)",
@@ -641,7 +656,7 @@ def run_render(args, rank, world, device):
     if rank != 0:
         return None
     pk = peaks()
-    falg = falg_per_query(c["space"])
+    falg = falg_per_query(c["space"], c["grad"])
     roof = roofline(args.config, falg, n, step_ms, step_ms, pk, r.prog.key)
     line = {
         "metric": "G reconstructions/sec per B200 (fraction of FP32 roofline in roofline)",

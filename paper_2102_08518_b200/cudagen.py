@@ -76,6 +76,7 @@ class GenConfig:
     rank: str = "match"          # sorted: rank in the psi class by "match" (warp-aggregated) | "atomic"
     presort: int = 0             # sorted: bin edge (cells) of a locality pre-sort of the queries (0 = off)
     tpairs: int = 1              # sorted + table + tloop: 2 = two pairs of one polynomial per thread
+    tchunk: int = 0              # table + tloop: monomials per pass (0 = all up to 96, else 80)
     cmajor: int = 0              # sorted: evaluate class by class (1; 2 = with a CTA barrier between
                                  # classes) so the warps of an SM execute one polynomial's code
     tloop: int = 0               # coeffs="table": 1 = a runtime loop over the stencil sites (code
@@ -487,6 +488,14 @@ class CudaProgram:
 
 
 DYN_TABLE_MIN = 40 * 1024     # sorted mode: larger shared tables live in dynamic shared memory
+
+
+def _monomial_chunks(nm: int, tchunk: int):
+    """Monomial ranges of the chunked table passes (multiples of 4 wide): one pass up to
+    96 monomials (order <= 3 in 3-D), else passes of about `tchunk` (0: 80)."""
+    size = tchunk or (nm if nm <= 96 else 80)
+    size = max(4, -(-size // 4) * 4)
+    return [(m0, min(nm, m0 + size)) for m0 in range(0, nm, size)]
 
 
 def _sigma_short(t: Tables) -> bool:
@@ -1753,6 +1762,9 @@ def generate(space, config: GenConfig | None = None, extents=None,
             L(f"const {vec}* __restrict__ Arow = reinterpret_cast<const {vec}*>(sg_A) + {psi_e};")
             if sctx.get("dual"):
                 return run_table_dual(nmp, midx, psi_e, vec, w, comps)
+            mchunks = _monomial_chunks(tab["nm"], cfg.tchunk) if cfg.tloop else [(0, tab["nm"])]
+            if len(mchunks) > 1:
+                return run_table_chunked(nmp, midx, psi_e, vec, w, comps, mchunks)
             for m in range(nmp):
                 L(f"{T} g{m} = ({T})0;")
             u = None
@@ -1833,26 +1845,56 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 em.indent = em.indent[:-2]
                 L("}")
 
-        def table_tail(nmp, midx, psi_e):
-            """acc (+ gacc) from the monomial coefficients g{m} in scope."""
-            if tab["has_free"]:
+        def run_table_chunked(nmp, midx, psi_e, vec, w, comps, mchunks):
+            """Site loop in passes over monomial ranges [m0, m1): each pass accumulates its
+            g_m over every site (the coefficient gathers of later passes hit L1) and folds
+            them into the value (+ gradient) by nested Horner over its own monomials, so
+            only m1 - m0 accumulators are live -- degree-9 pieces have 220 monomials."""
+            u = emit_u("")
+            nsite = (f"sg_npsi[{psi_e}]" if not t.uniform_n else str(t.n))
+            L(f"const int ns_ = {nsite};")
+            for m0, m1 in mchunks:
+                L("{")
+                em.indent += "  "
+                for m in range(m0, -(-m1 // w) * w):
+                    L(f"{T} g{m} = ({T})0;")
+                L(f"{T} cn_ = __ldg(V + (base + offt[0]));")
+                L("#pragma unroll 1")
+                L("for (int j_ = 0; j_ < ns_; ++j_) {")
+                L(f"  const {T} cj_ = cn_;")
+                L("  if (j_ + 1 < ns_) cn_ = __ldg(V + (base + offt[j_ + 1]));")
+                L(f"  const {vec}* __restrict__ Aj_ = Arow + j_ * {tab['nq'] * t.K};")
+                for q in range(m0 // w, -(-m1 // w)):
+                    L(f"  {{ const {vec} a_ = Aj_[{q * t.K}]; " + " ".join(
+                        f"g{q * w + r} = a_.{comps[r]} * cj_ + g{q * w + r};" for r in range(w)) + " }")
+                L("}")
+                table_tail(nmp, midx, psi_e, u=u, exps=tab["exps"][m0:m1], free=(m0 == 0))
+                em.indent = em.indent[:-2]
+                L("}")
+
+        def table_tail(nmp, midx, psi_e, u=None, exps=None, free=True):
+            """acc (+ gacc) from the monomial coefficients g{m} in scope (all monomials, or
+            the subset `exps` of one chunked pass)."""
+            exps = tab["exps"] if exps is None else list(exps)
+            eset = set(exps)
+            if tab["has_free"] and free:
                 L(f"const {T}* __restrict__ A0row = &sg_A0[{psi_e} * {nmp}];")
                 for m in range(tab["nm"]):
                     L(f"g{m} += A0row[{m}];")
-            u = emit_u("")
-            val = nested_horner(lambda e: f"g{midx[e]}" if e in midx else None, u)
+            u = emit_u("") if u is None else u
+            val = nested_horner(lambda e: f"g{midx[e]}" if e in eset else None, u, exps)
             L(f"acc += {val};")
             if cfg.grad:
                 du = []
                 for a in range(s):
                     def dcoef(e, a=a):
                         e2 = tuple(v + (k == a) for k, v in enumerate(e))
-                        if e2 not in midx:
+                        if e2 not in eset:
                             return None
                         f = e[a] + 1
                         return f"g{midx[e2]}" if f == 1 else f"{flit(f, fw)} * g{midx[e2]}"
                     dexps = sorted({tuple(v - (k == a) for k, v in enumerate(e))
-                                    for e in tab["exps"] if e[a] > 0})
+                                    for e in exps if e[a] > 0})
                     du.append(nested_horner(dcoef, u, dexps) if dexps else f"({T})0")
                 add_grad(du, True)
 

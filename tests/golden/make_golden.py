@@ -238,5 +238,67 @@ def main(argv):
     return 0
 
 
+
+
+# -- gradient work (bench configs that also return grad f) ---------------------------------
+
+
+def _tree_ops(node):
+    """fadd + fmul nodes of a reference Horner tree (what _tree_value emits, codegen.py:318-328)."""
+    from splinegen.poly import Add, Mul
+    if isinstance(node, (Add, Mul)):
+        return 1 + _tree_ops(node.left) + _tree_ops(node.right)
+    return 0
+
+
+def falg_gradient_extra(space, pts):
+    """FP ops per query the gradient adds to F_alg, by the reference's own counting rule:
+    for every (query, coset) the m=1 chunked greedy-Horner programs of the three partial
+    derivatives d psi / d u_k of the selected reference polynomial (the reference's
+    Poly.differentiate + group_polynomial + horner_factorize, poly.py:169-376; one fadd per
+    chunk accumulation as in _run_plan, codegen.py:332-356) plus grad_x = T^T grad_u
+    (3 x (3 fmul + 2 fadd) per coset).  The reference itself has no gradient program."""
+    from splinegen.poly import group_polynomial, horner_factorize
+    ops = []
+    for rp, sub0 in zip(space.ref_polys, [next(sb for sb in space.subregions if sb.psi_index == i)
+                                          for i in range(len(space.ref_polys))]):
+        total = 0
+        n = len(sub0.stencil)
+        for k in range(space.dim):
+            dp = rp.poly.differentiate(k)
+            cs = group_polynomial(dp, 1, range(n))
+            used = 0
+            for poly, _blk in cs.chunks:
+                if poly.terms:
+                    total += _tree_ops(horner_factorize(poly))
+                    used += 1
+            total += max(0, used - 1)
+        ops.append(total + space.dim * (2 * space.dim - 1))
+    acc = 0.0
+    for off in space.lattice.cosets:
+        xl = pts - np.array([float(q) for q in off])
+        _, xloc = ref_oracle._rho(space, xl)
+        sub = ref_oracle._membership(space, xloc)
+        psi = np.array([sb.psi_index for sb in space.subregions])[sub]
+        acc += float(np.array(ops)[psi].sum())
+    return acc / len(pts)
+
+
+def grad_main(names):
+    """falg.json["<space>+grad"] = F_alg + falg_gradient_extra, for the gradient configs."""
+    fpath = HERE / "falg.json"
+    falgs = json.loads(fpath.read_text())
+    for name in names:
+        text = (HERE / "spaces" / f"{name}.json").read_text()
+        space, _ = parse_extension_space(text)
+        z = np.load(HERE / f"{name}.npz")
+        pts = z["uniform_xs"].astype(np.float64)
+        falgs[f"{name}+grad"] = round(falgs[name] + falg_gradient_extra(space, pts), 3)
+        print(f"{name}+grad: {falgs[name + '+grad']:.2f} FP ops/query")
+    fpath.write_text(json.dumps(falgs, indent=1, sort_keys=True) + "\n")
+
+
 if __name__ == "__main__":
+    if sys.argv[1:2] == ["--grad"]:
+        raise SystemExit(grad_main(sys.argv[2:]))
     raise SystemExit(main(sys.argv[1:]))

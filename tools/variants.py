@@ -178,6 +178,13 @@ VARIANTS = {
     "c4_srt_sym_b512": dict(mode="sorted", block=512, coeffs="imm", form="sym"),
     "c4_direct_b256": dict(mode="direct", block=256, coeffs="imm"),
     "c4_direct_f64sel": dict(mode="direct", block=128, coeffs="imm", radix=1),
+    "tlc_b256": dict(mode="sorted", block=256, radix=1, coeffs="table", tloop=1),
+    "tlc_b512": dict(mode="sorted", block=512, radix=1, coeffs="table", tloop=1),
+    "tlc_b256_pre32": dict(mode="sorted", block=256, radix=1, coeffs="table", tloop=1, presort=32),
+    "tlc_b384_pre32": dict(mode="sorted", block=384, radix=1, coeffs="table", tloop=1, presort=32),
+    "tlc_b256_pre32_c56": dict(mode="sorted", block=256, radix=1, coeffs="table", tloop=1, presort=32, tchunk=56),
+    "tlc_b256_pre32_c112": dict(mode="sorted", block=256, radix=1, coeffs="table", tloop=1, presort=32, tchunk=112),
+    "tlc_b512_pre32_c56": dict(mode="sorted", block=512, radix=1, coeffs="table", tloop=1, presort=32, tchunk=56),
     "srt_imm_b128": dict(mode="sorted", block=128, radix=1, coeffs="imm"),
     "srt_imm_b256_t512": dict(mode="sorted", block=256, tile=512, radix=1, coeffs="imm"),
     "srt_imm_b256_t2048": dict(mode="sorted", block=256, tile=2048, radix=1, coeffs="imm"),
