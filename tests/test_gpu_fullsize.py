@@ -17,7 +17,7 @@ from paper_2102_08518_b200.model import SPACES_DIR  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
-CFGS = ["c1", "c2", "c3", "c4", "c4v", "c5", "c5u"]
+CFGS = ["c1", "c2", "c3", "c4", "c4v", "c4v4", "c5", "c5u"]
 NQ = 1 << 20
 
 
@@ -101,7 +101,7 @@ def test_multi_rank_bench_code_path():
     assert d["gather_ms"] is not None and d["gather_ms"] > 0
 
 
-SELECT_CFGS = ["c1", "c2", "c3", "c4", "c4v", "c5", "c5u", "c3o2"]
+SELECT_CFGS = ["c1", "c2", "c3", "c4", "c4v", "c4v4", "c5", "c5u", "c3o2"]
 
 
 @pytest.mark.parametrize("cfg", SELECT_CFGS)

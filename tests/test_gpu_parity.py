@@ -48,6 +48,8 @@ def _xs(z, which, dtype=torch.float32):
                                   "radix", "radix_f64", "presort"])
 def test_selection_bit_exact(name, mode):
     space, _, z, arrays = load_golden(name)
+    if _big(space) and mode not in ("sorted", "radix", "radix_f64", "presort"):
+        pytest.skip("variant not meant for order-4 spaces")
     if mode == "direct_f64":
         ev = _evaluator(space, arrays, dbg=True, select="f64")
     elif mode == "presort":
@@ -121,10 +123,23 @@ def _cfg(space, spec):
     return spec
 
 
+def _big(space):
+    """Order-4 spaces (thousands of terms per polynomial): only the variants meant for them
+    (sorted dispatch, branchy arms, table site loop) -- predicated immediates of 4 x 3,000
+    terms compile for minutes and spill."""
+    return max(len(rp.poly.terms) for rp in space.ref_polys) > 1500
+
+
+def _big_ok(spec):
+    return spec.get("mode") == "sorted" or spec.get("tloop") or spec.get("params_mode") == "branchy"
+
+
 @pytest.mark.parametrize("name", golden_names())
 @pytest.mark.parametrize("ci", range(len(CONFIGS)))
 def test_values_f32_vs_reference(name, ci):
     space, _, z, arrays = load_golden(name)
+    if _big(space) and not _big_ok(CONFIGS[ci]):
+        pytest.skip("variant not meant for order-4 spaces")
     ev = _evaluator(space, arrays, **_cfg(space, CONFIGS[ci]))
     for which in SETS:
         got = ev(_xs(z, which)).double().cpu().numpy()
@@ -136,6 +151,8 @@ def test_values_f32_vs_reference(name, ci):
 @pytest.mark.parametrize("name", golden_names())
 def test_values_f64_variant(name):
     space, _, z, arrays = load_golden(name)
+    if _big(space):
+        pytest.skip("f64 predicated immediates of order-4 spaces: see _big")
     for spec in (dict(), dict(params_mode="branchy", form="sites"), dict(unroll_cosets=False)):
         ev = _evaluator(space, arrays, float_width="f64", **_cfg(space, spec))
         for which in SETS:
@@ -147,9 +164,12 @@ def test_values_f64_variant(name):
 
 @pytest.mark.parametrize("name", golden_names())
 @pytest.mark.parametrize("mode", ["direct", "binned", "table", "sym", "sorted", "sorted_sym",
-                                  "pack2", "pack2_binned_sym", "presort", "sorted_table_pairs"])
+                                  "pack2", "pack2_binned_sym", "presort", "sorted_table_pairs",
+                                  "table_loop"])
 def test_gradient_vs_oracle(name, mode):
     space, ospace, z, arrays = load_golden(name)
+    if _big(space) and mode not in ("sorted_table_pairs", "table_loop"):
+        pytest.skip("variant not meant for order-4 spaces")
     xs = z["uniform_xs"].astype(np.float64)
     _, gwant = refeval.reference_eval_batch(ospace, xs, [a.astype(np.float64) for a in arrays],
                                             grad=True)
@@ -163,7 +183,11 @@ def test_gradient_vs_oracle(name, mode):
         ev = _evaluator(space, arrays, grad=True, pack=2)
     elif mode == "presort":
         ev = _evaluator(space, arrays, grad=True, mode="sorted", presort=4)
+    elif mode == "table_loop":
+        ev = _evaluator(space, arrays, grad=True, mode="sorted", coeffs="table", tloop=1, block=256)
     elif mode == "sorted_table_pairs":
+        if _big(space):
+            pytest.skip("two pairs per thread need one monomial pass")
         ev = _evaluator(space, arrays, grad=True, mode="sorted", coeffs="table", tloop=1, tpairs=2,
                         block=256)
     elif mode == "pack2_binned_sym":
@@ -180,6 +204,8 @@ def test_gradient_vs_oracle(name, mode):
 @pytest.mark.parametrize("mode", ["direct", "binned", "sorted", "pack2", "presort"])
 def test_host_path_matches_device_path(name, mode):
     space, _, z, arrays = load_golden(name)
+    if _big(space) and mode != "sorted":
+        pytest.skip("variant not meant for order-4 spaces")
     if mode == "pack2":
         ev = _evaluator(space, arrays, pack=2)
     elif mode == "presort":
