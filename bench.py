@@ -67,7 +67,7 @@ CONFIGS = {
                 desc="FCC Voronoi spline (order 2), 4x161^3, 2^26 uniform, value + gradient"),
     "c4v": dict(space="fcc_voronoi3", extents=(161, 161, 161), queries=1 << 26, kind="uniform",
                  grad=True, scaling="weak",
-                 variant=dict(mode="sorted", coeffs="imm", form="sym", block=512, radix=1, presort=32),
+                 variant=dict(mode="sorted", coeffs="imm", form="sym", block=512, radix=1, presort=16),
                  desc="FCC Voronoi spline (order 3, the paper's FCC case), 4x161^3, 2^26 uniform, "
                       "value + gradient"),
     "c4v4": dict(space="fcc_voronoi4", extents=(161, 161, 161), queries=1 << 26, kind="uniform",
@@ -76,10 +76,11 @@ CONFIGS = {
                               presort=32),
                  desc="FCC Voronoi spline (order 4, 'cubic'), 4x161^3, 2^26 uniform, value + gradient"),
     "c5u": dict(space="bcc_voronoi3", extents=(406, 406, 406), queries=1 << 30, kind="uniform",
-                grad=False, scaling="strong",
-                variant=dict(mode="binned", stage="l1", block=256, bin=136, coeffs="imm"),
+                grad=False, scaling="strong", steps=20,
+                variant=dict(mode="sorted", coeffs="imm", block=640, tile=3200, radix=1, min_blocks=1,
+                             cmajor=3, presort=64),
                 desc="c5 with uniform random queries (SURVEY 8d secondary): 535 MB volume > L2; "
-                     "a coarse locality sort (136-cell bins, no bricks) keeps the gathers in L2"),
+                     "a locality pre-sort of the queries (64-cell bins) keeps the gathers in L2"),
     "c3r": dict(space="bcc_voronoi3", extents=(203, 203, 203), queries=1 << 26, kind="render",
                 rays=(512, 512, 256), grad=False, scaling="weak", variant=dict(),
                 desc="fused volume render of c3: 512x512 rays x 256 samples through 2x203^3 BCC "

@@ -185,6 +185,10 @@ VARIANTS = {
     "tlc_b256_pre32_c56": dict(mode="sorted", block=256, radix=1, coeffs="table", tloop=1, presort=32, tchunk=56),
     "tlc_b256_pre32_c112": dict(mode="sorted", block=256, radix=1, coeffs="table", tloop=1, presort=32, tchunk=112),
     "tlc_b512_pre32_c56": dict(mode="sorted", block=512, radix=1, coeffs="table", tloop=1, presort=32, tchunk=56),
+    "u_cm3_pre136": dict(mode="sorted", block=640, tile=3200, radix=1, coeffs="imm", min_blocks=1, cmajor=3, presort=136),
+    "u_cm3_pre64": dict(mode="sorted", block=640, tile=3200, radix=1, coeffs="imm", min_blocks=1, cmajor=3, presort=64),
+    "u_cm3_pre32": dict(mode="sorted", block=640, tile=3200, radix=1, coeffs="imm", min_blocks=1, cmajor=3, presort=32),
+    "u_cm3": dict(mode="sorted", block=640, tile=3200, radix=1, coeffs="imm", min_blocks=1, cmajor=3),
     "srt_imm_b128": dict(mode="sorted", block=128, radix=1, coeffs="imm"),
     "srt_imm_b256_t512": dict(mode="sorted", block=256, tile=512, radix=1, coeffs="imm"),
     "srt_imm_b256_t2048": dict(mode="sorted", block=256, tile=2048, radix=1, coeffs="imm"),
