@@ -272,6 +272,18 @@ class Volume:
         self.handle = h
         self.ncosets = len(arrs)
 
+    def replicate(self, device: int, stream=None) -> "Volume":
+        """A full copy of this volume (halo included) on `device`: a peer copy over NVLink
+        between GPUs, a device-to-device copy on the same GPU (sg_volume_replicate) -- how
+        every rank of a multi-GPU run gets its replica without a host round trip."""
+        h = ctypes.c_void_p()
+        _check(lib().sg_volume_replicate(self.handle, int(device), _stream_ptr(stream, self.device),
+                                         ctypes.byref(h)))
+        r = Volume.__new__(Volume)
+        r.dtype, r.dim, r.extents, r.halo = self.dtype, self.dim, self.extents, self.halo
+        r.device, r.ncosets, r.handle = int(device), self.ncosets, h
+        return r
+
     @property
     def nbytes(self):
         b = ctypes.c_int64()

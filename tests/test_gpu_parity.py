@@ -345,3 +345,31 @@ def test_persistent_modules_on_two_streams(kind):
         launch_b(sb)
         torch.cuda.synchronize()
         assert torch.equal(r.rgba, want_a) and torch.equal(rgba_b, want_b)
+
+
+def test_volume_replicate():
+    """sg_volume_replicate: the replica (same GPU here; a peer copy over NVLink across GPUs
+    when more than one is visible) evaluates bit-identically to the original."""
+    from paper_2102_08518_b200 import runtime
+    space, _, z, arrays = load_golden("bcc_voronoi3" if "bcc_voronoi3" in golden_names() else "bcc_box5")
+    ev = _evaluator(space, arrays, mode="sorted", radix=1)
+    xs = torch.from_numpy(z["uniform_xs"]).cuda()
+    want = ev(xs)
+    devs = list(range(torch.cuda.device_count()))
+    for dev in devs[:2]:
+        rep = ev.volume.replicate(dev)
+        assert rep.nbytes == ev.volume.nbytes
+        if dev == ev.device:
+            out = torch.empty_like(want)
+            runtime.eval_device(ev.module, rep, xs, out)
+            torch.cuda.synchronize()
+            assert torch.equal(out, want)
+        else:
+            from paper_2102_08518_b200.runtime import Module
+            mod = Module(ev.prog, dev)
+            with torch.cuda.device(dev):
+                x2 = xs.to(f"cuda:{dev}")
+                out = torch.empty(x2.shape[0], device=f"cuda:{dev}")
+                runtime.eval_device(mod, rep, x2, out)
+                torch.cuda.synchronize(dev)
+            assert torch.equal(out.cpu(), want.cpu())
