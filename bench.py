@@ -11,12 +11,16 @@ host call (`sg_eval_host`: H2D of the queries from pinned memory, kernel, D2H
 of the results, every step).
 
 Configs (BASELINE.json, restated concretely in SURVEY.md 8d):
-  c1  tricubic B-spline on Z^3, 64^3, 2^20 uniform queries
-  c2  BCC quintic box spline, 2 x 101^3 coset-split, 2^24 uniform queries  (default)
-  c3  BCC Voronoi spline (order 2), 2 x 203^3, 2^26 ray-ordered queries
-  c4  FCC 6-direction box spline, 4 x 161^3, 2^26 uniform queries, value + gradient
-  c4v FCC Voronoi spline (order 2), 4 x 161^3, 2^26 uniform queries, value + gradient
-  c5  BCC Voronoi spline, 2 x 406^3, 2^30 ray-ordered queries (strong-scaled over the GPUs)
+  c1   tricubic B-spline on Z^3, 64^3, 2^20 uniform queries
+  c2   BCC quintic box spline, 2 x 101^3 coset-split, 2^24 uniform queries
+  c3   BCC Voronoi spline (order 3), 2 x 203^3, 2^26 ray-ordered queries
+  c4   FCC 6-direction box spline, 4 x 161^3, 2^26 uniform queries, value + gradient
+  c4v  FCC Voronoi spline (order 3), 4 x 161^3, 2^26 uniform queries, value + gradient
+  c4v4 FCC Voronoi spline (order 4, "cubic"), 4 x 161^3, 2^26 uniform, value + gradient
+  c5   BCC Voronoi spline (order 3), 2 x 406^3, 2^30 ray-ordered queries, strong-scaled over
+       the GPUs (default: the largest single-GPU configuration)
+  c5u  c5 with uniform queries; c3r / c3rs the fused renderer of c3 (without / with shading);
+  c3o2 / c4vo2 / c5o2 the order-2 Voronoi versions measured in round 1
 Under torchrun every rank evaluates its own batch (weak scaling, volume replicated).
 """
 
