@@ -15,6 +15,7 @@ for c in $CFGS; do
     -o gpurun_out/prof_${c}_${TAG} -f python bench.py --config $c --steps 3 --warmup 3 --no-cpu > gpurun_out/ncu_${c}_${TAG}.log 2>&1
   python tools/ncu_extract.py $c gpurun_out/prof_${c}_${TAG}.ncu-rep $TAG > /dev/null 2>&1 && cp profiles/ncu_${c}.json gpurun_out/
   python tools/ncu_summary.py gpurun_out/prof_${c}_${TAG}.ncu-rep > gpurun_out/${TAG}_ncu_${c}_summary.txt 2>&1
+  rm -f gpurun_out/prof_${c}_${TAG}.ncu-rep   # gpurun copies back <= 64 MiB: keep the summaries only
   timeout 1200 python bench.py --config $c > gpurun_out/${TAG}_bench_${c}.json 2> gpurun_out/${TAG}_bench_${c}.err
   echo "$c: $(head -c 300 gpurun_out/${TAG}_bench_${c}.json)"
 done

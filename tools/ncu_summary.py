@@ -53,7 +53,27 @@ def raw(path):
     return recs
 
 
+def table(paths):
+    """Side-by-side key metrics of several single-kernel reports (knob pairs)."""
+    import os
+    recs = [raw(p)[0] for p in paths]
+    names = [os.path.basename(p).replace(".ncu-rep", "")[-24:] for p in paths]
+    print(f"{'metric':64s}" + "".join(f"{n:>26s}" for n in names))
+    for k in KEYS:
+        if all(k in r for r in recs):
+            print(f"{k[:64]:64s}" + "".join(f"{r[k][0]:>26s}" for r in recs))
+    for r, n in zip(recs, names):
+        tot = sum(float(v.replace(',', '')) for k, (v, u) in r.items()
+                  if k.startswith(STALL2) and v not in ('', 'n/a') and not k.endswith("_not_issued"))
+        st = sorted(((float(v.replace(',', '')) if v not in ('', 'n/a') else 0.0, k)
+                     for k, (v, u) in r.items() if k.startswith(STALL2)
+                     and not k.endswith("_not_issued")), reverse=True)[:6]
+        print(f"stalls {n}: " + ", ".join(f"{k[len(STALL2):]}={v / max(tot, 1):.0%}" for v, k in st))
+
+
 def main():
+    if len(sys.argv) > 2 and sys.argv[1] == "--table":
+        return table(sys.argv[2:])
     for path in sys.argv[1:]:
         for rec in raw(path):
             print(f"== {path}  {rec.get('Kernel Name', ('?',))[0][:40]}")

@@ -50,6 +50,8 @@ VARIANTS = {
     "imm_pred": dict(coeffs="imm"),
     "direct": dict(mode="direct", block=128),
     "sym": dict(form="sym"),
+    "horner": dict(form="horner"),
+    "horner_table": dict(form="horner", coeffs="table"),
     "f64sel": dict(select="f64"),
     "sorted": dict(mode="sorted", block=256),
     "sorted_sym": dict(mode="sorted", form="sym", block=256),
@@ -177,6 +179,7 @@ VARIANTS = {
     "c4_srt": dict(mode="sorted", block=256, coeffs="imm"),
     "c4_srt_sym_b512": dict(mode="sorted", block=512, coeffs="imm", form="sym"),
     "c4_direct_b256": dict(mode="direct", block=256, coeffs="imm"),
+    "c4_direct_b128": dict(mode="direct", block=128, coeffs="imm"),
     "c4_direct_f64sel": dict(mode="direct", block=128, coeffs="imm", radix=1),
     "tlc_b256": dict(mode="sorted", block=256, radix=1, coeffs="table", tloop=1),
     "tlc_b512": dict(mode="sorted", block=512, radix=1, coeffs="table", tloop=1),
