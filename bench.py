@@ -49,6 +49,10 @@ CONFIGS = {
     "c1": dict(space="tricubic", extents=(64, 64, 64), queries=1 << 20, kind="uniform",
                grad=False, scaling="weak", variant=dict(mode="binned", form="sym"),
                desc="tensor-product tricubic B-spline on Z^3, 64^3, 2^20 uniform"),
+    "c1l": dict(space="tricubic", extents=(64, 64, 64), queries=1 << 20, kind="uniform",
+                grad=False, scaling="weak", variant=dict(mode="direct", fetch="linear", block=256),
+                desc="c1 through the hardware linear-fetch variant (SURVEY 8f row f4: 8 filtered "
+                     "texture fetches instead of 64 reads; opt-in, ~3e-3 accurate, not the 1e-5 bar)"),
     "c2": dict(space="bcc_box5", extents=(101, 101, 101), queries=1 << 24, kind="uniform",
                grad=False, scaling="weak",
                variant=dict(mode="binned", coeffs="imm", form="sym", block=512),

@@ -90,7 +90,12 @@ typedef struct sg_module_info {
   int32_t presort;
 } sg_module_info;
 
-enum { SG_MODE_DIRECT = 0, SG_MODE_BINNED = 1, SG_MODE_RENDER = 2 };
+/* SG_MODE_LINEAR: tensor-product kernels that fetch
+ * pairs of neighbouring coefficients with ONE hardware-filtered texture read.  The library
+ * binds one f32 texture per coset (cudaArray copy of the volume, wrap addressing, linear
+ * filtering), built on the first launch against a volume; 8-bit filter weights make the
+ * results ~1e-3 accurate -- opt-in, never the default. */
+enum { SG_MODE_DIRECT = 0, SG_MODE_BINNED = 1, SG_MODE_RENDER = 2, SG_MODE_LINEAR = 3 };
 enum { SG_FLOOR = 0, SG_ROUND = 1 };
 
 int sg_version(void);

@@ -212,7 +212,77 @@ struct sg_volume {
   size_t bytes = 0;
   size_t coset_off[SG_MAX_COSETS] = {};  // byte offset of each coset's padded array
   const void* origin[SG_MAX_COSETS] = {};  // padded element (h, h, ..., h)
+  // linear-fetch modules (SG_MODE_LINEAR): one filtered, wrapping f32 texture per coset,
+  // built from the volume on first use (volume_textures) and owned by the volume
+  cudaArray_t tarr[SG_MAX_COSETS] = {};
+  unsigned long long tex[SG_MAX_COSETS] = {};
+  bool tex_ready = false;
 };
+
+struct SgTex {  // must match linfetch.py
+  unsigned long long t[SG_MAX_COSETS];
+};
+
+static std::mutex g_tex_mu;
+
+static void volume_textures_free(sg_volume* v) {
+  for (int c = 0; c < SG_MAX_COSETS; ++c) {
+    if (v->tex[c]) cudaDestroyTextureObject((cudaTextureObject_t)v->tex[c]);
+    if (v->tarr[c]) cudaFreeArray(v->tarr[c]);
+    v->tex[c] = 0;
+    v->tarr[c] = nullptr;
+  }
+  v->tex_ready = false;
+}
+
+// Texture objects of a volume (built once): the unpadded coset arrays are copied from the
+// padded allocation into cudaArrays (axis s-1 -> texture x), sampled with normalized
+// coordinates, wrap addressing (the reference's periodic fetch) and linear filtering.
+static int volume_textures(sg_volume* v, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(g_tex_mu);
+  if (v->tex_ready) return SG_OK;
+  if (v->dtype != SG_F32 || v->dim > 3)
+    return fail(SG_EINVAL, "linear fetch needs an f32 volume of dimension <= 3");
+  for (int c = 0; c < v->ncosets; ++c) {
+    const int s = v->dim;
+    const size_t w = (size_t)v->ext[c][s - 1];
+    const size_t h = s >= 2 ? (size_t)v->ext[c][s - 2] : 0;
+    const size_t d = s >= 3 ? (size_t)v->ext[c][s - 3] : 0;
+    cudaChannelFormatDesc desc = cudaCreateChannelDesc<float>();
+    cudaError_t e = cudaMalloc3DArray(&v->tarr[c], &desc, make_cudaExtent(w, h, d));
+    if (e != cudaSuccess) {
+      volume_textures_free(v);
+      return fail(SG_ENOMEM, "cudaMalloc3DArray: %s", cudaGetErrorString(e));
+    }
+    cudaMemcpy3DParms p{};
+    const size_t pw = (size_t)v->pext[c][s - 1];
+    const size_t ph = s >= 2 ? (size_t)v->pext[c][s - 2] : 1;
+    p.srcPtr = make_cudaPitchedPtr(const_cast<void*>(v->origin[c]), pw * sizeof(float), w, ph);
+    p.dstArray = v->tarr[c];
+    p.extent = make_cudaExtent(w, h ? h : 1, d ? d : 1);
+    p.kind = cudaMemcpyDeviceToDevice;
+    e = cudaMemcpy3DAsync(&p, st);
+    if (e == cudaSuccess) {
+      cudaResourceDesc rd{};
+      rd.resType = cudaResourceTypeArray;
+      rd.res.array.array = v->tarr[c];
+      cudaTextureDesc td{};
+      for (int a = 0; a < 3; ++a) td.addressMode[a] = cudaAddressModeWrap;
+      td.filterMode = cudaFilterModeLinear;
+      td.readMode = cudaReadModeElementType;
+      td.normalizedCoords = 1;
+      cudaTextureObject_t t = 0;
+      e = cudaCreateTextureObject(&t, &rd, &td, nullptr);
+      v->tex[c] = (unsigned long long)t;
+    }
+    if (e != cudaSuccess) {
+      volume_textures_free(v);
+      return fail(SG_ECUDA, "volume texture: %s", cudaGetErrorString(e));
+    }
+  }
+  v->tex_ready = true;
+  return SG_OK;
+}
 
 // Periodic ghost-halo fill: dst (padded, C order) <- src (unpadded, C order).
 template <typename T>
@@ -652,6 +722,11 @@ int sg_module_load(const void* image, size_t image_len, const char* entry, int d
       }
     }
   }
+  if (m->info.mode == SG_MODE_LINEAR && (m->info.dtype != SG_F32 || m->info.dim > 3)) {
+    cudaLibraryUnload(m->lib);
+    delete m;
+    return fail(SG_EINVAL, "linear-fetch modules filter f32 volumes of dimension <= 3");
+  }
   if (m->info.mode == SG_MODE_DIRECT && m->info.presort) {
     if (m->info.dtype != SG_F32 || m->info.dim > 3 || m->info.bin < 1) {
       cudaLibraryUnload(m->lib);
@@ -852,6 +927,7 @@ int sg_volume_create(int device, int dim, int ncosets, const int64_t* extents, i
 int sg_volume_free(sg_volume* v) {
   if (!v) return SG_OK;
   cudaSetDevice(v->device);
+  volume_textures_free(v);
   if (v->alloc) cudaFree(v->alloc);
   delete v;
   return SG_OK;
@@ -874,6 +950,11 @@ int sg_volume_replicate(const sg_volume* v, int device, void* stream, sg_volume*
   CU(cudaSetDevice(device));
   sg_volume* r = new sg_volume(*v);
   r->device = device;
+  for (int c = 0; c < SG_MAX_COSETS; ++c) {   // textures are per volume: rebuilt on use
+    r->tarr[c] = nullptr;
+    r->tex[c] = 0;
+  }
+  r->tex_ready = false;
   cudaError_t e = cudaMalloc(&r->alloc, r->bytes);
   if (e != cudaSuccess) {
     delete r;
@@ -1132,10 +1213,17 @@ static int launch(sg_module* m, const sg_volume* v, const void* xs, int64_t n, v
   }
   SgCosets cs{};
   for (int c = 0; c < v->ncosets; ++c) cs.base[c] = v->origin[c];
+  SgTex tx{};
+  const bool linear = m->info.mode == SG_MODE_LINEAR;
+  if (linear) {
+    int rt = volume_textures(const_cast<sg_volume*>(v), st);
+    if (rt) return rt;
+    for (int c = 0; c < v->ncosets; ++c) tx.t[c] = v->tex[c];
+  }
   long long nn = (long long)n;
   unsigned* err = nullptr;
   void* args[] = {(void*)&xs, (void*)&nn, (void*)&out, (void*)&grad, (void*)&dbg, (void*)&err,
-                  (void*)&cs};
+                  linear ? (void*)&tx : (void*)&cs};
   long long per_block = (long long)m->info.block * m->info.queries_per_thread;
   long long grid = (nn + per_block - 1) / per_block;
   int sms = 148;

@@ -82,11 +82,16 @@ class GenConfig:
     tloop: int = 0               # coeffs="table": 1 = a runtime loop over the stencil sites (code
                                  # shared by every reference polynomial: no instruction-cache
                                  # pressure for large polynomials), 0 = fully unrolled
+    fetch: str = "point"         # "linear": hardware-filtered texture fetches for tensor-product
+                                 # spaces (opt-in, ~1e-3 accurate: linfetch.py)
 
     def __post_init__(self):
         if self.float_width is None:
             object.__setattr__(self, "float_width",
-                               F64 if (self.mode == "direct" and self.pack == 1) else F32)
+                               F64 if (self.mode == "direct" and self.pack == 1
+                                       and self.fetch == "point") else F32)
+        if self.fetch not in ("point", "linear"):
+            raise ValueError("fetch must be 'point' or 'linear'")
         if self.float_width not in (F64, F32):
             raise ValueError(f"float width must be f64 or f32, not {self.float_width!r}")
         if self.form not in FORMS:
@@ -579,6 +584,9 @@ def generate(space, config: GenConfig | None = None, extents=None,
         else tuple(tuple(int(v) for v in extents) for _ in range(M))
     if len(ext) != M or any(len(e) != s for e in ext):
         raise ValueError(f"extents must give {s} values for each of {M} cosets")
+    if cfg.fetch == "linear":
+        from .linfetch import generate_linear
+        return generate_linear(space, cfg, ext)
     h = t.halo
     binned = cfg.mode == "binned"
     render = cfg.mode == "render"

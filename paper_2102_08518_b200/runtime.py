@@ -187,7 +187,7 @@ class Module:
         for c, row in enumerate(prog.padded_extents):
             for d, e in enumerate(row):
                 info.padded_extents[c][d] = e
-        info.mode = {"binned": 1, "render": 2}.get(prog.mode, 0)
+        info.mode = {"binned": 1, "render": 2, "linear": 3}.get(prog.mode, 0)
         info.rounding = prog.rounding
         info.stage_tma = int(prog.stage_tma)
         info.smem_bytes = prog.smem_bytes

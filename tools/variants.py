@@ -51,6 +51,8 @@ VARIANTS = {
     "direct": dict(mode="direct", block=128),
     "sym": dict(form="sym"),
     "horner": dict(form="horner"),
+    "linear": dict(mode="direct", fetch="linear", block=256),
+    "linear_b128": dict(mode="direct", fetch="linear", block=128),
     "horner_table": dict(form="horner", coeffs="table"),
     "f64sel": dict(select="f64"),
     "sorted": dict(mode="sorted", block=256),
