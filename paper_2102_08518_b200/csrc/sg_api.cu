@@ -666,8 +666,8 @@ int sg_compile(const char* source, const char* name, const char* const* opts, in
 
 int sg_module_load(const void* image, size_t image_len, const char* entry, int device,
                    const sg_module_info* info, sg_module** out) {
-  (void)image_len;
   if (!image || !entry || !info || !out) return fail(SG_EINVAL, "NULL argument");
+  if (image_len < 16) return fail(SG_EINVAL, "image of %zu bytes is not a cubin", image_len);
   if (info->dim < 1 || info->dim > SG_MAX_DIM) return fail(SG_EINVAL, "bad dim %d", info->dim);
   if (info->ncosets < 1 || info->ncosets > SG_MAX_COSETS)
     return fail(SG_EINVAL, "bad coset count %d", info->ncosets);

@@ -433,13 +433,24 @@ class Producer:
             return self._norm
         s = self.s
         lo, hi = self.phi.support_box()
-        x = tuple(F(self.rng.randint(-400, 400), 997) for _ in range(s))
-        tot = F(0)
-        rngs = [range(math.floor(-float(hi[d])) - 1, math.ceil(-float(lo[d])) + 2) for d in range(s)]
-        for c in self.cosets:
-            for n in itertools.product(*rngs):
-                tot += self.phi(tuple(x[d] - c[d] - n[d] for d in range(s)))
-        self._norm = 1 / tot
+        rngs = [range(math.floor(-float(hi[d])) - 2, math.ceil(-float(lo[d])) + 3) for d in range(s)]
+        # generic points: coordinate d is k_d / P_d with distinct primes P_d and k_d != 0 mod P_d,
+        # so no shifted copy x - c - n lies on a knot plane (a.x = o with small integer a and
+        # dyadic o has no such solution) -- a point on a knot plane made the exact box-spline
+        # sum wrong (fcc_voronoi3 once shipped a reference polynomial scaled by 1/41.9)
+        primes = (997, 1009, 1013, 1019, 1021, 1031)
+        tots = []
+        for _ in range(2):
+            x = tuple(F(self.rng.choice([v for v in range(-400, 401) if v]), primes[d % len(primes)])
+                      for d in range(s))
+            tot = F(0)
+            for c in self.cosets:
+                for n in itertools.product(*rngs):
+                    tot += self.phi(tuple(x[d] - c[d] - n[d] for d in range(s)))
+            tots.append(tot)
+        if tots[0] != tots[1] or tots[0] <= 0:
+            raise RuntimeError(f"phi is not a partition of unity up to scale: {tots}")
+        self._norm = 1 / tots[0]
         return self._norm
 
     # 6. sigma + assembly ----------------------------------------------------------------

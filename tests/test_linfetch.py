@@ -20,10 +20,12 @@ from tests.gpu_util import load_golden
 
 SEPARABLE = {"tricubic": (8, 64), "trilinear": (1, 8), "linear1d": (1, 2)}
 
-# |error| per filtered fetch <= (number of filtered axes) x max|c_{a+1} - c_a| / 512
-# (8-bit lerp fraction, round to nearest); the stencil weights are >= 0 and sum to 1, so
-# for coefficients in [0, 1) the value error is below 3/512 plus fp32 rounding.
-FILTER_BOUND = 3.0 / 512 + 1e-5
+# |error| per filtered fetch <= (number of filtered axes) x max|c_{a+1} - c_a| / 256
+# (the texture unit's 8-bit lerp fraction; the B200 measured 5.89e-3 on trilinear, just above
+# the 3/512 a round-to-nearest fraction would give, so the bound assumes truncation); the
+# stencil weights are >= 0 and sum to 1, so for coefficients in [0, 1) the value error is
+# below 3/256 plus fp32 rounding.
+FILTER_BOUND = 3.0 / 256 + 1e-5
 
 
 def _cfg(space, **kw):
@@ -84,7 +86,8 @@ def _run(space, arrays, xs, **kw):
 
     from paper_2102_08518_b200 import Evaluator
     ev = Evaluator(space, [a.astype(np.float32) for a in arrays], _cfg(space, **kw))
-    out, _, dbg = ev(torch.from_numpy(xs).cuda())
+    res = ev(torch.from_numpy(xs).cuda())
+    out, dbg = (res[0], res[-1]) if isinstance(res, tuple) else (res, None)
     torch.cuda.synchronize()
     ev.module.status()
     return out.double().cpu().numpy(), (None if dbg is None else dbg.cpu().numpy())

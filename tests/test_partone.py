@@ -99,3 +99,49 @@ def test_fixture_listing():
     names = list_fixtures()
     for n in ("tricubic", "bcc_box5"):
         assert n in names
+
+
+def _shipped_spaces():
+    from paper_2102_08518_b200.model import SPACES_DIR
+    return sorted(p.stem for p in SPACES_DIR.glob("*.json"))
+
+
+@pytest.mark.parametrize("name", _shipped_spaces())
+def test_every_shipped_space_is_a_partition_of_unity(name):
+    """All-ones data reconstruct 1 everywhere (reference tests/test_acceptance.py:86-93) for
+    every space the package ships, checked through the oracle on the space file itself: a
+    reference polynomial with a wrong scale (the producer once normalized one fit on a
+    knot-plane point, fcc_voronoi3) shows up here before any GPU run."""
+    from paper_2102_08518_b200.model import SPACES_DIR
+    osp = refeval.load_space_file(SPACES_DIR / f"{name}.json")
+    ext = (6,) * osp.dim
+    rng = np.random.default_rng(17)
+    xs = rng.random((400, osp.dim)) * 6 - 1.5
+    ones = [np.ones(ext) for _ in range(osp.ncosets)]
+    assert np.abs(refeval.reference_eval_batch(osp, xs, ones) - 1).max() <= 1e-9
+
+
+VORONOI_EXACT = {"bcc_voronoi2": ("bcc", 2, 4), "fcc_voronoi2": ("fcc", 2, 6), "fcc_voronoi3": ("fcc", 3, 3)}
+
+
+@pytest.mark.parametrize("name", sorted(VORONOI_EXACT))
+def test_voronoi_tables_match_exact_phi(name):
+    """The produced tables reproduce the Voronoi spline exactly: phi(y)
+    through the space's sub-region tables (oracle basis_from_delta_batch) equals the exact
+    rational box-spline sum V_k(y) / vol(V)^(k-1) (the partition-of-unity scale) at generic
+    rational points spread over the support."""
+    from paper_2102_08518_b200.model import SPACES_DIR
+    from paper_2102_08518_b200.partone.voronoi import (BCC_VORONOI_GENS, FCC_VORONOI_GENS,
+                                                       voronoi_spline, zonotope_volume)
+    lat, order, npts = VORONOI_EXACT[name]
+    gens = BCC_VORONOI_GENS if lat == "bcc" else FCC_VORONOI_GENS
+    phi = voronoi_spline(gens, order)
+    scale = 1 / zonotope_volume(gens) ** (order - 1)
+    osp = refeval.load_space_file(SPACES_DIR / f"{name}.json")
+    rng = np.random.default_rng(23)
+    ys = [tuple(F(int(rng.integers(-600, 600)) or 1, p) for p in (997, 1009, 1013))
+          for _ in range(npts)]
+    got = refeval.basis_from_delta_batch(osp, np.array([[float(v) for v in y] for y in ys]))
+    want = np.array([float(scale * phi(y)) for y in ys])
+    assert np.any(want > 1e-3)
+    assert np.abs(got - want).max() <= 1e-12

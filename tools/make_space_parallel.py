@@ -47,13 +47,20 @@ def main():
     p.orbits()
     p.reps_all = list(p.reps)
     _P = p
+    # checkpoint of the fits, keyed by the representatives' sign vectors: a checkpoint from a
+    # run whose orbit representatives differ must not be reused (it would attach every fit to
+    # the wrong reference region)
+    reps_key = [p.region_list[i].q for i in p.reps_all]
     ck = Path(f"/tmp/{name}_fits.pkl")
+    res = None
     if ck.exists():
-        res = pickle.loads(ck.read_bytes())
-    else:
+        saved = pickle.loads(ck.read_bytes())
+        if isinstance(saved, dict) and saved.get("reps") == reps_key:
+            res = saved["fits"]
+    if res is None:
         with mp.get_context("fork").Pool(workers) as pool:
             res = sorted(pool.map(_fit_one, range(len(p.reps_all)), chunksize=1))
-        ck.write_bytes(pickle.dumps(res))
+        ck.write_bytes(pickle.dumps({"reps": reps_key, "fits": res}))
     p.reps = p.reps_all
     p.ref_polys = [r[1] for r in res]
     p.ref_stencils = [r[2] for r in res]
