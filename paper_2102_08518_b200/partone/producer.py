@@ -432,6 +432,13 @@ class Producer:
         if hasattr(self, "_norm"):
             return self._norm
         s = self.s
+        known = getattr(self.phi, "lattice_sum", None)
+        if known is not None and self.phi.degree() > 6:
+            # order >= 4 Voronoi splines: one exact point value costs ~30 s, a lattice sum
+            # hours; the closed form is used and the shipped space's partition of unity is
+            # checked afterwards through its tables (tests/test_partone.py)
+            self._norm = 1 / known
+            return self._norm
         lo, hi = self.phi.support_box()
         rngs = [range(math.floor(-float(hi[d])) - 2, math.ceil(-float(lo[d])) + 3) for d in range(s)]
         # generic points: coordinate d is k_d / P_d with distinct primes P_d and k_d != 0 mod P_d,
@@ -448,8 +455,8 @@ class Producer:
                 for n in itertools.product(*rngs):
                     tot += self.phi(tuple(x[d] - c[d] - n[d] for d in range(s)))
             tots.append(tot)
-        if tots[0] != tots[1] or tots[0] <= 0:
-            raise RuntimeError(f"phi is not a partition of unity up to scale: {tots}")
+        if tots[0] != tots[1] or tots[0] <= 0 or (known is not None and tots[0] != known):
+            raise RuntimeError(f"phi is not a partition of unity up to scale: {tots} (closed form {known})")
         self._norm = 1 / tots[0]
         return self._norm
 

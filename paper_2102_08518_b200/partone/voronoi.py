@@ -92,6 +92,9 @@ def voronoi_spline(gens, order: int) -> BoxSum:
     out = BoxSum(s, terms)
     # support of V_k: the zonotope of every generator taken k times, centred at 0
     out.hull = (tuple(gens), tuple([order] * len(gens)), tuple(-order * c for c in center))
+    # sum over the lattice whose Voronoi cell is Z(gens): the translates of chi_V tile space,
+    # so sum_n (chi_V * V_{k-1})(x - n) = integral of V_{k-1} = vol(V)^(k-1), exactly
+    out.lattice_sum = zonotope_volume(gens) ** (order - 1)
     return out
 
 

@@ -204,6 +204,20 @@ VARIANTS = {
     "srt_pre64": dict(mode="sorted", block=512, radix=1, coeffs="imm", presort=64),
     "srt_pre16": dict(mode="sorted", block=512, radix=1, coeffs="imm", presort=16),
     "srt_sym_pre32": dict(mode="sorted", block=512, radix=1, coeffs="imm", form="sym", presort=32),
+    "c4_l1_bin16": dict(mode="binned", stage="l1", block=256, bin=16),
+    "c4_l1_bin32": dict(mode="binned", stage="l1", block=256, bin=32),
+    "c4_l1_bin32_b128": dict(mode="binned", stage="l1", block=128, bin=32),
+    "c4_srt_pre16": dict(mode="sorted", block=256, coeffs="imm", presort=16, radix=1),
+    "c4_srt_pre32": dict(mode="sorted", block=256, coeffs="imm", presort=32, radix=1),
+    "c4_srt_sym_pre16": dict(mode="sorted", block=512, coeffs="imm", form="sym", presort=16, radix=1),
+    "c4_srt_sym_pre32": dict(mode="sorted", block=512, coeffs="imm", form="sym", presort=32, radix=1),
+    "c4_direct_pre": dict(mode="direct", block=128, coeffs="imm"),
+    "nopre": dict(presort=0),
+    "nopre_b256": dict(presort=0, block=256),
+    "nopre_horner": dict(presort=0, form="horner"),
+    "nopre_cm3": dict(presort=0, cmajor=3),
+    "nopre_cm3_b640_t3200": dict(presort=0, cmajor=3, block=640, tile=3200, min_blocks=1),
+    "pre8": dict(presort=8),
     "l1_bin32_imm": dict(mode="binned", stage="l1", block=256, bin=32, coeffs="imm", branchy=True),
     "l1_bin32_table": dict(mode="binned", stage="l1", block=256, bin=32, coeffs="table"),
 }
