@@ -75,6 +75,8 @@ class GenConfig:
     radix: int = 0               # 1: sub-region via a mixed-radix index of the plane-family counts
     rank: str = "match"          # sorted: rank in the psi class by "match" (warp-aggregated) | "atomic"
     presort: int = 0             # sorted: bin edge (cells) of a locality pre-sort of the queries (0 = off)
+    presort_chunk: int = 0       # presort: log2 of the queries per locality chunk (0 = one chunk);
+                                 # results are then scattered inside one chunk's window at a time
     tpairs: int = 1              # sorted + table + tloop: 2 = two pairs of one polynomial per thread
     tchunk: int = 0              # table + tloop: monomials per pass (0 = all up to 96, else 80)
     cmajor: int = 0              # sorted: evaluate class by class (1; 2 = with a CTA barrier between
@@ -82,6 +84,8 @@ class GenConfig:
     tloop: int = 0               # coeffs="table": 1 = a runtime loop over the stencil sites (code
                                  # shared by every reference polynomial: no instruction-cache
                                  # pressure for large polynomials), 0 = fully unrolled
+    fetch_offsets: str = "affine"  # sorted mode, per-polynomial stencils: "affine" (offsets from
+                                   # the arm's reference stencil + 4 ints per sub-region) | "table"
     fetch: str = "point"         # "linear": hardware-filtered texture fetches for tensor-product
                                  # spaces (opt-in, ~1e-3 accurate: linfetch.py)
 
@@ -92,6 +96,8 @@ class GenConfig:
                                        and self.fetch == "point") else F32)
         if self.fetch not in ("point", "linear"):
             raise ValueError("fetch must be 'point' or 'linear'")
+        if self.fetch_offsets not in ("affine", "table"):
+            raise ValueError("fetch_offsets must be 'affine' or 'table'")
         if self.float_width not in (F64, F32):
             raise ValueError(f"float width must be f64 or f32, not {self.float_width!r}")
         if self.form not in FORMS:
@@ -169,6 +175,10 @@ class Tables:
     affine: list | None     # per sub: (A int s x s, b int s) with pi_sub[j] = A ref[j] + b
     ref_stencil: list       # n x s
     n_psi: list = None      # K: stencil size of each reference polynomial (n = the largest)
+    # per reference polynomial its stencil (that of its first sub-region) and per sub-region
+    # (A, b) with pi_sub[j] = A ref_psi[psi_sub][j] + b (None when some sub has no such map)
+    ref_psi: list = None
+    paffine: list | None = None
 
     @property
     def uniform_n(self):
@@ -255,6 +265,17 @@ def derive_tables(space: SplineSpace) -> Tables:
     n_psi = [0] * len(space.ref_polys)
     for sb in subs:
         n_psi[sb.psi_index] = len(sb.stencil)
+    ref_psi = [None] * len(space.ref_polys)
+    for st, p_ in zip(stencils, psi):
+        if ref_psi[p_] is None:
+            ref_psi[p_] = st
+    paff = []
+    for st, p_ in zip(stencils, psi):
+        r = _solve_affine(ref_psi[p_], st, s) if len(st) == len(ref_psi[p_]) else None
+        if r is None:
+            paff = None
+            break
+        paff.append(r)
     P = space.indexer.modulus
     Q = len(space.planes)
     return Tables(
@@ -265,7 +286,7 @@ def derive_tables(space: SplineSpace) -> Tables:
         transforms=transforms, tshift=tshift, stencils=stencils, psi=psi, halo=halo,
         uniform_T=len(set(transforms)) == 1, uniform_tp=len(set(tshift)) == 1,
         uniform_stencil=len({tuple(x) for x in stencils}) == 1, uniform_psi=len(set(psi)) == 1,
-        affine=aff, ref_stencil=ref, n_psi=n_psi)
+        affine=aff, ref_stencil=ref, n_psi=n_psi, ref_psi=ref_psi, paffine=paff)
 
 
 def plane_families(t: Tables) -> dict:
@@ -479,6 +500,7 @@ class CudaProgram:
     chunk: int = 0
     queries_per_thread: int = 1   # sorted mode: tile / block (one CTA tile per grid step)
     presort: int = 0              # bin edge of the C ABI's locality pre-sort (sorted mode)
+    presort_chunk: int = 0        # log2 queries per locality chunk of that sort (0 = one chunk)
     stage_tma: bool = False
     rounding: int = 1
     meta: dict = field(default_factory=dict)
@@ -599,6 +621,8 @@ def generate(space, config: GenConfig | None = None, extents=None,
         raise ValueError("presort applies to mode='sorted' (query kernels)")
     if presort and (s > 3 or len(set(ext)) != 1):
         raise ValueError("presort needs equal coset extents and dimension <= 3")
+    if cfg.presort_chunk and not (presort and 10 <= cfg.presort_chunk <= 30):
+        raise ValueError("presort_chunk (log2 queries per locality chunk) needs presort and 10..30")
     pack2 = cfg.pack == 2
     if pack2:
         if cfg.float_width != F32 or cfg.mode not in ("direct", "binned"):
@@ -750,7 +774,8 @@ def generate(space, config: GenConfig | None = None, extents=None,
       f"form={cfg.form} coeffs={cfg.coeffs} {fw} block={cfg.block} grad={int(cfg.grad)} "
       f"dbg={int(cfg.dbg)}")
     A(f"// extents={ext} stencil reach={h} padded={pext[0]} halo={H} mode={cfg.mode}"
-      + (f" bin={bin_} brick={tuple(brick)} stage={cfg.stage}" if binned else ""))
+      + (f" bin={bin_} brick={tuple(brick)} stage={cfg.stage}" if binned else "")
+      + (f" presort={presort} presort_chunk={cfg.presort_chunk}" if presort else ""))
     A("struct SgCosets { const void* base[8]; };")
     A("template <typename T> __device__ __forceinline__ void sg_st(T* p, T v) { *p = v; }")
     if binned:
@@ -805,15 +830,22 @@ def generate(space, config: GenConfig | None = None, extents=None,
         if not t.uniform_tp:
             smem.append(("sg_tp", T, [float(v) for tp in t.tshift for v in tp]))
     fetch_mode = "uniform" if t.uniform_stencil else ("affine" if t.affine is not None else "table")
+    if (fetch_mode == "table" and t.paffine is not None and sorted_ and cfg.coeffs != "table"
+            and cfg.fetch_offsets == "affine"):
+        # sorted dispatch evaluates one reference polynomial per arm, so its fetch offsets
+        # can be boff + sum_e m_j[e] sp_e with the polynomial's own reference stencil m as
+        # compile-time constants: one int4 load per pair instead of one (bank-conflicted)
+        # table load per stencil site
+        fetch_mode = "paffine"
     if cfg.tloop:
         fetch_mode = "table"      # the site loop reads its offsets from the per-sub-region table
     if fetch_mode != "uniform" and not same_geom and not cfg.unroll_cosets:
         pass  # per-coset strides are compile-time constants in unrolled mode only; handled below
-    if fetch_mode == "affine":
+    if fetch_mode in ("affine", "paffine"):
         # per geometry g: S'_sub = A_sub^T S (s ints) and boff_sub = b_sub . S
         for g, st in enumerate(strides if not same_geom else strides[:1]):
             vals = []
-            for A_, b_ in t.affine:
+            for A_, b_ in (t.affine if fetch_mode == "affine" else t.paffine):
                 sp = [sum(A_[d][e] * st[d] for d in range(s)) for e in range(s)]
                 vals += sp + [sum(b_[d] * st[d] for d in range(s))]
             smem.append((f"sg_aff{g}", "int", vals))
@@ -1528,7 +1560,32 @@ def generate(space, config: GenConfig | None = None, extents=None,
             return
         L = em.line
         # ---- per-sub fetch offsets
-        if fetch_mode == "affine":
+        if fetch_mode == "paffine":
+            gi = 0 if same_geom else geo
+            if s == 3:
+                L(f"const int4 aff = *reinterpret_cast<const int4*>(&sg_aff{gi}[sub * 4]);")
+                for e, comp in zip(range(3), "xyz"):
+                    L(f"const int sp{e} = aff.{comp};")
+                L("const int boff = base + aff.w;")
+            else:
+                L(f"const int* aff = &sg_aff{gi}[sub * {s + 1}];")
+                for e in range(s):
+                    L(f"const int sp{e} = aff[{e}];")
+                L(f"const int boff = base + aff[{s}];")
+
+            def off_expr(j):
+                site = t.ref_psi[sctx["cur_psi"]][j]
+                parts = ["boff"]
+                for e in range(s):
+                    v = site[e]
+                    if v == 1:
+                        parts.append(f"sp{e}")
+                    elif v == -1:
+                        parts.append(f"-sp{e}")
+                    elif v:
+                        parts.append(f"{v} * sp{e}")
+                return " + ".join(parts).replace("+ -", "- ")
+        elif fetch_mode == "affine":
             gi = 0 if same_geom else geo
             if s == 3:
                 L(f"const int4 aff = *reinterpret_cast<const int4*>(&sg_aff{gi}[sub * 4]);")
@@ -1914,6 +1971,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
             for i in range(t.K):
                 L(f"{'default' if i == t.K - 1 else f'case {i}'}: {{")
                 em.indent += "  "
+                sctx["cur_psi"] = i
                 accs, grads, _ = run_plan([i], f"_{i}")
                 L(f"acc += {accs[i]};")
                 if cfg.grad:
@@ -2479,6 +2537,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
         chunk=cfg.chunk if binned else 0,
         queries_per_thread=cfg.tile // cfg.block if sorted_ else 1,
         presort=presort,
+        presort_chunk=cfg.presort_chunk if presort else 0,
         rounding=(0 if (rm0.shape == PARALLELEPIPED and rm0.rounding == "floor") else 1),
         meta={"fetch_mode": fetch_mode, "K": t.K, "nsub": t.nsub, "n": t.n, "reach": h,
               "smem_tables": [x[0] for x in smem], "lut_entries": len(lut)})
