@@ -88,11 +88,6 @@ typedef struct sg_module_info {
    * queries by cubes of `bin` cells (the binned-mode sort, for locality only) and the
    * kernel reads the (x, y, z, original index) records, writing results by index */
   int32_t presort;
-  /* presort modules: log2 of the queries per locality chunk (0 = one chunk).  The sort key
-   * is (chunk of the original index, bin): results are written by index inside one chunk's
-   * window at a time, so the scattered result stores of uniform random queries merge in L2
-   * instead of costing a DRAM read-modify-write per 4-B store */
-  int32_t presort_chunk_log2;
 } sg_module_info;
 
 /* SG_MODE_LINEAR: tensor-product kernels that fetch

@@ -103,7 +103,6 @@ struct sg_module {
   cudaEvent_t bin_done = nullptr;
   void* bin_scratch = nullptr;
   size_t bin_scratch_bytes = 0;
-  size_t bin_head_zeroed = 0;   // bytes of the scratch head known to be zero (bin totals)
   int64_t nbins = 0;
   int64_t nb[SG_MAX_DIM] = {1, 1, 1, 1};
   // optional event timing of the evaluation kernel
@@ -326,8 +325,7 @@ struct BinGeom {
   float inv_ext[3];
   float inv_bin;
   int nb[3];
-  long long nbins;       // bins per locality chunk
-  int ctas_per_chunk;    // sort CTAs (contiguous query ranges) per locality chunk
+  long long nbins;
 };
 
 
@@ -381,9 +379,7 @@ __global__ void __launch_bounds__(SG_SORT_THREADS) sg_bin_count(
     const float* __restrict__ xs, long long n, long long per, BinGeom g,
     int* __restrict__ mat, int* __restrict__ bin_tot) {
   extern __shared__ int hist[];
-  // locality chunks: the CTAs of one chunk (ctas_per_chunk consecutive ranges) count into
-  // that chunk's bins of the totals
-  int* __restrict__ tot = bin_tot + (long long)(blockIdx.x / g.ctas_per_chunk) * g.nbins;
+  const int G = gridDim.x;
   for (int b = threadIdx.x; b < g.nbins; b += blockDim.x) hist[b] = 0;
   __syncthreads();
   const long long lo = (long long)blockIdx.x * per;
@@ -394,8 +390,8 @@ __global__ void __launch_bounds__(SG_SORT_THREADS) sg_bin_count(
   __syncthreads();
   for (int b = threadIdx.x; b < g.nbins; b += blockDim.x) {
     const int h = hist[b];
-    mat[(long long)blockIdx.x * g.nbins + b] = h;   // CTA-major: coalesced, per-chunk bins
-    if (h) atomicAdd(&tot[b], h);
+    mat[(long long)b * G + blockIdx.x] = h;
+    if (h) atomicAdd(&bin_tot[b], h);
   }
 }
 
@@ -468,10 +464,10 @@ __global__ void __launch_bounds__(SG_SORT_THREADS) sg_bin_scatter(
     const int* __restrict__ mat, int* __restrict__ cursor, float4* __restrict__ sorted) {
   extern __shared__ int sh[];
   int* cnt = sh;   // running position per bin: this CTA's reserved range in each bin
-  int* __restrict__ cur = cursor + (long long)(blockIdx.x / g.ctas_per_chunk) * g.nbins;
+  const int G = gridDim.x;
   for (int b = threadIdx.x; b < g.nbins; b += blockDim.x) {
-    const int c = mat[(long long)blockIdx.x * g.nbins + b];
-    cnt[b] = c ? atomicAdd(&cur[b], c) : 0;
+    const int c = mat[(long long)b * G + blockIdx.x];
+    cnt[b] = c ? atomicAdd(&cursor[b], c) : 0;
   }
   __syncthreads();
   const long long lo = (long long)blockIdx.x * per;
@@ -501,10 +497,10 @@ __global__ void __launch_bounds__(THREADS) sg_bin_scatter_tiled(
   int* loff = lcnt + nb;                                           // nb: tile offsets
   int* gbase = loff + nb;                                          // nb: this tile's global base
   __shared__ int scan_sh[32];
-  int* __restrict__ cur = cursor + (long long)(blockIdx.x / g.ctas_per_chunk) * nb;
+  const int G = gridDim.x;
   for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-    const int c = mat[(long long)blockIdx.x * nb + b];
-    gpos[b] = c ? atomicAdd(&cur[b], c) : 0;
+    const int c = mat[(long long)b * G + blockIdx.x];
+    gpos[b] = c ? atomicAdd(&cursor[b], c) : 0;
     lcnt[b] = 0;
   }
   __syncthreads();
@@ -1044,52 +1040,30 @@ static int sort_queries(sg_module* m, const void* xs, int64_t n, cudaStream_t st
   int scatter_groups = scatter_groups_env > 0 ? scatter_groups_env : 1;
   if (!((scatter_threads == 512 && scatter_groups == 2) || (scatter_threads == 256 && scatter_groups == 4)))
     scatter_groups = 1;
-  long long G_ = G;
-  long long per = ((n + G_ - 1) / G_ + 3) & ~3LL;   // multiple of 4: float4 query groups
-  // locality chunks (presort modules): the sort key is (chunk of the original query index,
-  // bin); a chunk is a whole number of sort-CTA ranges, so every CTA counts and scatters
-  // into one chunk's bins
-  long long cpc = G_, nchunks = 1;
-  if (in.presort && in.presort_chunk_log2 > 0 && in.presort_chunk_log2 < 40 &&
-      (1LL << in.presort_chunk_log2) < n) {
-    const long long cq = 1LL << in.presort_chunk_log2;
-    cpc = std::max<long long>(1, (cq + per - 1) / per);
-    per = ((cq + cpc - 1) / cpc + 3) & ~3LL;
-    G_ = (n + per - 1) / per;
-    nchunks = (G_ + cpc - 1) / cpc;
-  }
-  const size_t nbt = nb * (size_t)nchunks;   // bins over all chunks
-  const long long mlen = (long long)nb * G_;
+  const long long per = ((n + G - 1) / G + 3) & ~3LL;   // multiple of 4: float4 query groups
+  const long long mlen = (long long)nb * G;
   const int chunk = std::max(32, in.chunk);
-  const long long max_items = (n + chunk - 1) / chunk + (long long)nbt;
+  const long long max_items = (n + chunk - 1) / chunk + (long long)nb;
   // layout: bin totals (kept zero between calls) | cursors | starts | count matrix | items | records
-  const size_t head = ((3 * nbt + 1) * sizeof(int) + 15) & ~(size_t)15;
+  const size_t head = ((3 * nb + 1) * sizeof(int) + 15) & ~(size_t)15;
   const size_t need = head + (((size_t)mlen * sizeof(int) + 15) & ~(size_t)15) +
                       (size_t)max_items * sizeof(int2) + (size_t)n * sizeof(float4) + 512;
-  if (!m->bin_done) CU(cudaEventCreateWithFlags(&m->bin_done, cudaEventDisableTiming));
-  CU(cudaStreamWaitEvent(st, m->bin_done, 0));   // the previous launch has released the scratch
   if (m->bin_scratch_bytes < need) {
-    if (m->bin_scratch) {
-      CU(cudaStreamSynchronize(st));
-      cudaFree(m->bin_scratch);
-    }
+    if (m->bin_scratch) cudaFree(m->bin_scratch);
     m->bin_scratch = nullptr;
     m->bin_scratch_bytes = 0;
-    m->bin_head_zeroed = 0;
     CU(cudaMalloc(&m->bin_scratch, need));
+    CU(cudaMemset(m->bin_scratch, 0, head));
     m->bin_scratch_bytes = need;
   }
-  if (m->bin_head_zeroed < head) {
-    // the totals must start at zero (sg_bin_plan re-zeroes the ones it consumed)
-    CU(cudaMemsetAsync(m->bin_scratch, 0, head, st));
-    m->bin_head_zeroed = head;
-  }
   int* bin_tot = (int*)m->bin_scratch;
-  int* cursor = bin_tot + nbt;
-  int* starts = cursor + nbt;
+  int* cursor = bin_tot + nb;
+  int* starts = cursor + nb;
   int* mat = (int*)((char*)m->bin_scratch + head);
   int2* items = (int2*)((char*)mat + (((size_t)mlen * sizeof(int) + 15) & ~(size_t)15));
   float4* sorted = (float4*)(((uintptr_t)(items + max_items) + 255) & ~(uintptr_t)255);
+  if (!m->bin_done) CU(cudaEventCreateWithFlags(&m->bin_done, cudaEventDisableTiming));
+  CU(cudaStreamWaitEvent(st, m->bin_done, 0));   // the previous launch has released the scratch
   BinGeom g{};
   g.dim = in.dim;
   g.bin = in.bin;
@@ -1100,7 +1074,6 @@ static int sort_queries(sg_module* m, const void* xs, int64_t n, cudaStream_t st
     g.nb[d] = d < in.dim ? (int)m->nb[d] : 1;
   }
   g.nbins = (long long)nb;
-  g.ctas_per_chunk = (int)cpc;
   static std::once_flag attr_once;
   std::call_once(attr_once, [] {
     cudaFuncSetAttribute(sg_bin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1119,10 +1092,10 @@ static int sort_queries(sg_module* m, const void* xs, int64_t n, cudaStream_t st
     cudaFuncSetAttribute(sg_bin_scatter_tiled<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          4096 * (sizeof(float4) + sizeof(int)) + tb);
   });
-  sg_bin_count<<<(unsigned)G_, SG_SORT_THREADS, nb * sizeof(int), st>>>((const float*)xs, (long long)n,
-                                                                       per, g, mat, bin_tot);
+  sg_bin_count<<<(unsigned)G, SG_SORT_THREADS, nb * sizeof(int), st>>>((const float*)xs, (long long)n,
+                                                                      per, g, mat, bin_tot);
   CU(cudaGetLastError());
-  sg_bin_plan<<<1, 1024, 0, st>>>(bin_tot, (int)nbt, (long long)n, chunk, starts, cursor, items,
+  sg_bin_plan<<<1, 1024, 0, st>>>(bin_tot, (int)nb, (long long)n, chunk, starts, cursor, items,
                                   (int)max_items);
   CU(cudaGetLastError());
   if (nb <= (size_t)SG_TILED_MAX_BINS) {
@@ -1130,17 +1103,17 @@ static int sort_queries(sg_module* m, const void* xs, int64_t n, cudaStream_t st
                        4 * nb * sizeof(int);
     const float* xq = (const float*)xs;
     if (scatter_threads == 256 && scatter_groups == 4)
-      sg_bin_scatter_tiled<256, 4><<<(unsigned)G_, 256, shb, st>>>(xq, (long long)n, per, g, mat, cursor, sorted);
+      sg_bin_scatter_tiled<256, 4><<<(unsigned)G, 256, shb, st>>>(xq, (long long)n, per, g, mat, cursor, sorted);
     else if (scatter_threads == 256)
-      sg_bin_scatter_tiled<256, 1><<<(unsigned)G_, 256, shb, st>>>(xq, (long long)n, per, g, mat, cursor, sorted);
+      sg_bin_scatter_tiled<256, 1><<<(unsigned)G, 256, shb, st>>>(xq, (long long)n, per, g, mat, cursor, sorted);
     else if (scatter_threads == 512 && scatter_groups == 2)
-      sg_bin_scatter_tiled<512, 2><<<(unsigned)G_, 512, shb, st>>>(xq, (long long)n, per, g, mat, cursor, sorted);
+      sg_bin_scatter_tiled<512, 2><<<(unsigned)G, 512, shb, st>>>(xq, (long long)n, per, g, mat, cursor, sorted);
     else if (scatter_threads == 512)
-      sg_bin_scatter_tiled<512, 1><<<(unsigned)G_, 512, shb, st>>>(xq, (long long)n, per, g, mat, cursor, sorted);
+      sg_bin_scatter_tiled<512, 1><<<(unsigned)G, 512, shb, st>>>(xq, (long long)n, per, g, mat, cursor, sorted);
     else
-      sg_bin_scatter_tiled<1024, 1><<<(unsigned)G_, 1024, shb, st>>>(xq, (long long)n, per, g, mat, cursor, sorted);
+      sg_bin_scatter_tiled<1024, 1><<<(unsigned)G, 1024, shb, st>>>(xq, (long long)n, per, g, mat, cursor, sorted);
   } else {
-    sg_bin_scatter<<<(unsigned)G_, SG_SORT_THREADS, nb * sizeof(int), st>>>(
+    sg_bin_scatter<<<(unsigned)G, SG_SORT_THREADS, nb * sizeof(int), st>>>(
         (const float*)xs, (long long)n, per, g, mat, cursor, sorted);
   }
   CU(cudaGetLastError());

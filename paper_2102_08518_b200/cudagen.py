@@ -75,8 +75,6 @@ class GenConfig:
     radix: int = 0               # 1: sub-region via a mixed-radix index of the plane-family counts
     rank: str = "match"          # sorted: rank in the psi class by "match" (warp-aggregated) | "atomic"
     presort: int = 0             # sorted: bin edge (cells) of a locality pre-sort of the queries (0 = off)
-    presort_chunk: int = 0       # presort: log2 of the queries per locality chunk (0 = one chunk);
-                                 # results are then scattered inside one chunk's window at a time
     tpairs: int = 1              # sorted + table + tloop: 2 = two pairs of one polynomial per thread
     tchunk: int = 0              # table + tloop: monomials per pass (0 = all up to 96, else 80)
     cmajor: int = 0              # sorted: evaluate class by class (1; 2 = with a CTA barrier between
@@ -500,7 +498,6 @@ class CudaProgram:
     chunk: int = 0
     queries_per_thread: int = 1   # sorted mode: tile / block (one CTA tile per grid step)
     presort: int = 0              # bin edge of the C ABI's locality pre-sort (sorted mode)
-    presort_chunk: int = 0        # log2 queries per locality chunk of that sort (0 = one chunk)
     stage_tma: bool = False
     rounding: int = 1
     meta: dict = field(default_factory=dict)
@@ -621,8 +618,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
         raise ValueError("presort applies to mode='sorted' (query kernels)")
     if presort and (s > 3 or len(set(ext)) != 1):
         raise ValueError("presort needs equal coset extents and dimension <= 3")
-    if cfg.presort_chunk and not (presort and 10 <= cfg.presort_chunk <= 30):
-        raise ValueError("presort_chunk (log2 queries per locality chunk) needs presort and 10..30")
+
     pack2 = cfg.pack == 2
     if pack2:
         if cfg.float_width != F32 or cfg.mode not in ("direct", "binned"):
@@ -775,7 +771,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
       f"dbg={int(cfg.dbg)}")
     A(f"// extents={ext} stencil reach={h} padded={pext[0]} halo={H} mode={cfg.mode}"
       + (f" bin={bin_} brick={tuple(brick)} stage={cfg.stage}" if binned else "")
-      + (f" presort={presort} presort_chunk={cfg.presort_chunk}" if presort else ""))
+      + (f" presort={presort}" if presort else ""))
     A("struct SgCosets { const void* base[8]; };")
     A("template <typename T> __device__ __forceinline__ void sg_st(T* p, T v) { *p = v; }")
     if binned:
@@ -2537,7 +2533,6 @@ def generate(space, config: GenConfig | None = None, extents=None,
         chunk=cfg.chunk if binned else 0,
         queries_per_thread=cfg.tile // cfg.block if sorted_ else 1,
         presort=presort,
-        presort_chunk=cfg.presort_chunk if presort else 0,
         rounding=(0 if (rm0.shape == PARALLELEPIPED and rm0.rounding == "floor") else 1),
         meta={"fetch_mode": fetch_mode, "K": t.K, "nsub": t.nsub, "n": t.n, "reach": h,
               "smem_tables": [x[0] for x in smem], "lut_entries": len(lut)})

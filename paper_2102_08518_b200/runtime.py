@@ -48,8 +48,7 @@ class sg_module_info(ctypes.Structure):
                 ("stage_tma", ctypes.c_int32), ("smem_bytes", ctypes.c_int32),
                 ("bin", ctypes.c_int32), ("brick", ctypes.c_int32 * SG_MAX_DIM),
                 ("extents", ctypes.c_int64 * SG_MAX_DIM), ("chunk", ctypes.c_int32),
-                ("static_smem", ctypes.c_int32), ("presort", ctypes.c_int32),
-                ("presort_chunk_log2", ctypes.c_int32)]
+                ("static_smem", ctypes.c_int32), ("presort", ctypes.c_int32)]
 
 
 _lib = None
@@ -201,7 +200,6 @@ class Module:
         if getattr(prog, "presort", 0):
             info.presort = 1
             info.bin = prog.presort
-            info.presort_chunk_log2 = getattr(prog, "presort_chunk", 0)
             info.chunk = 1 << 16        # the sort's work-item list is unused here: keep it short
         h = ctypes.c_void_p()
         buf = ctypes.create_string_buffer(self.image, len(self.image))

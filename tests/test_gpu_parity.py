@@ -45,17 +45,15 @@ def _xs(z, which, dtype=torch.float32):
 
 @pytest.mark.parametrize("name", golden_names())
 @pytest.mark.parametrize("mode", ["direct", "binned", "sorted", "direct_f64", "pack2", "pack2_binned",
-                                  "radix", "radix_f64", "presort", "presort_chunked"])
+                                  "radix", "radix_f64"', "presort"])
 def test_selection_bit_exact(name, mode):
     space, _, z, arrays = load_golden(name)
-    if _big(space) and mode not in ("sorted", "radix", "radix_f64", "presort", "presort_chunked"):
+    if _big(space) and mode not in ("sorted", "radix", "radix_f64", "presort"):
         pytest.skip("variant not meant for order-4 spaces")
     if mode == "direct_f64":
         ev = _evaluator(space, arrays, dbg=True, select="f64")
     elif mode == "presort":
         ev = _evaluator(space, arrays, dbg=True, mode="sorted", presort=4)
-    elif mode == "presort_chunked":
-        ev = _evaluator(space, arrays, dbg=True, mode="sorted", presort=4, presort_chunk=10)
     elif mode.startswith("radix"):
         ev = _evaluator(space, arrays, dbg=True, radix=1, mode="sorted",
                         select="f64" if mode.endswith("f64") else "auto")
@@ -99,7 +97,6 @@ CONFIGS = [
     dict(mode="sorted", rank="atomic", radix=1),
     dict(mode="sorted", presort=4, radix=1),
     dict(mode="sorted", presort=8, form="sym", tile=512, block=256),
-    dict(mode="sorted", presort=4, presort_chunk=10, radix=1),
     dict(pack=2, mode="binned", form="sym"),
     dict(pack=2, form="sites", params_md=(2, 4)),
     dict(pack=2, mode="binned", block=256, select="f64"),

@@ -226,17 +226,6 @@ VARIANTS = {
     "cm3_tl_b640_t1920": dict(coeffs="table", tloop=1, cmajor=3, block=640, tile=1920, min_blocks=1),
     "cm3_tl_b512_t2048_c42": dict(coeffs="table", tloop=1, cmajor=3, block=512, tile=2048, min_blocks=1, tchunk=42),
     "tl_b512_t2048": dict(coeffs="table", tloop=1, cmajor=0, block=512, tile=2048, min_blocks=1),
-    "ch18": dict(presort_chunk=18),
-    "ch19": dict(presort_chunk=19),
-    "ch20": dict(presort_chunk=20),
-    "ch21": dict(presort_chunk=21),
-    "ch22": dict(presort_chunk=22),
-    "pre8_ch20": dict(presort=8, presort_chunk=20),
-    "pre32_ch20": dict(presort=32, presort_chunk=20),
-    "c4_srt_pre16_ch20": dict(mode="sorted", block=256, coeffs="imm", presort=16, radix=1, presort_chunk=20),
-    "c4_srt_pre16_ch21": dict(mode="sorted", block=256, coeffs="imm", presort=16, radix=1, presort_chunk=21),
-    "c4_srt_sym_pre16_ch20": dict(mode="sorted", block=512, coeffs="imm", form="sym", presort=16, radix=1, presort_chunk=20),
-    "c4_srt_pre8_ch20": dict(mode="sorted", block=256, coeffs="imm", presort=8, radix=1, presort_chunk=20),
     "l1_bin32_imm": dict(mode="binned", stage="l1", block=256, bin=32, coeffs="imm", branchy=True),
     "l1_bin32_table": dict(mode="binned", stage="l1", block=256, bin=32, coeffs="table"),
 }
