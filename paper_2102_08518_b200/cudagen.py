@@ -2004,6 +2004,80 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 em.indent = em.indent[:-2]
             L("}")
 
+    def neg2(x):
+        return f"make_float2(-({x}).x, -({x}).y)"
+
+    def pair_value(i, U, C, want_grad):
+        """(value pair, [grad pairs]) of reference polynomial i, packed float2 (FFMA2) for
+        pack=2 (two queries per thread)."""
+        L = em.line
+        f = symforms[i] if symforms is not None else None
+        if f is None:
+            if symforms is not None:
+                node_list = [horner_factorize(space.ref_polys[i].poly)]
+            else:
+                node_list = [tr for tr in trees[i] if tr is not None]
+            val = None
+            for nd in node_list:
+                v = em.tree2(nd, U, C)
+                if val is None:
+                    val = v
+                else:
+                    nt = em.tmp("p")
+                    L(f"const float2 {nt} = __fadd2_rn({val}, {v});")
+                    val = nt
+            val = val or "make_float2(0.f, 0.f)"
+            gr = None
+            if want_grad:
+                gr = [em.tree2(gtrees[i][a], U, C) if gtrees[i][a] is not None
+                      else "make_float2(0.f, 0.f)" for a in range(s)]
+            return val, gr
+        vv = []
+        for d in range(s):
+            if f.shift[d] != 0:
+                nm = em.tmp("p")
+                z = flit(-f.shift[d], F32)
+                L(f"const float2 {nm} = __fadd2_rn({U[d]}, make_float2({z}, {z}));")
+                vv.append(nm)
+            else:
+                vv.append(U[d])
+        sv = [None] * len(f.mixes)
+        kk = len(f.axes)
+        for reps, syms in f.orbits:
+            if len(reps) == 1 << kk:
+                x = {bits: C[j] for bits, j in reps}
+                for tb in range(kk):
+                    nx = {}
+                    for b in x:
+                        if b >> tb & 1:
+                            continue
+                        hi_ = b | (1 << tb)
+                        a_, b_ = em.tmp("p"), em.tmp("p")
+                        L(f"const float2 {a_} = __fadd2_rn({x[b]}, {x[hi_]});")
+                        L(f"const float2 {b_} = __fadd2_rn({x[b]}, {neg2(x[hi_])});")
+                        nx[b], nx[hi_] = a_, b_
+                    x = nx
+                for P, k_ in syms.items():
+                    sv[k_] = x[P]
+            else:
+                for P, k_ in syms.items():
+                    expr = None
+                    for sign, j in f.mixes[k_]:
+                        term = C[j] if sign > 0 else neg2(C[j])
+                        if expr is None:
+                            expr = term
+                        else:
+                            nm = em.tmp("p")
+                            L(f"const float2 {nm} = __fadd2_rn({expr}, {term});")
+                            expr = nm
+                    sv[k_] = expr
+        val = em.tree2(sym_trees[i], vv, sv)
+        gr = None
+        if want_grad:
+            gr = [em.tree2(sym_gtrees[i][a], vv, sv) if sym_gtrees[i][a] is not None
+                  else "make_float2(0.f, 0.f)" for a in range(s)]
+        return val, gr
+
     def emit_pack2_body():
         """pack=2: two queries per thread.  Selection, fetch and u stay scalar per query
         (in their own scopes); the polynomial evaluation runs once on float2 pairs, so
@@ -2050,78 +2124,6 @@ def generate(space, config: GenConfig | None = None, extents=None,
         em.lines = []
         em.indent = "  "
         L = em.line
-
-        def neg2(x):
-            return f"make_float2(-({x}).x, -({x}).y)"
-
-        def pair_value(i, U, C, want_grad):
-            """(value pair, [grad pairs]) of reference polynomial i."""
-            f = symforms[i] if symforms is not None else None
-            if f is None:
-                if symforms is not None:
-                    node_list = [horner_factorize(space.ref_polys[i].poly)]
-                else:
-                    node_list = [tr for tr in trees[i] if tr is not None]
-                val = None
-                for nd in node_list:
-                    v = em.tree2(nd, U, C)
-                    if val is None:
-                        val = v
-                    else:
-                        nt = em.tmp("p")
-                        L(f"const float2 {nt} = __fadd2_rn({val}, {v});")
-                        val = nt
-                val = val or "make_float2(0.f, 0.f)"
-                gr = None
-                if want_grad:
-                    gr = [em.tree2(gtrees[i][a], U, C) if gtrees[i][a] is not None
-                          else "make_float2(0.f, 0.f)" for a in range(s)]
-                return val, gr
-            vv = []
-            for d in range(s):
-                if f.shift[d] != 0:
-                    nm = em.tmp("p")
-                    z = flit(-f.shift[d], F32)
-                    L(f"const float2 {nm} = __fadd2_rn({U[d]}, make_float2({z}, {z}));")
-                    vv.append(nm)
-                else:
-                    vv.append(U[d])
-            sv = [None] * len(f.mixes)
-            kk = len(f.axes)
-            for reps, syms in f.orbits:
-                if len(reps) == 1 << kk:
-                    x = {bits: C[j] for bits, j in reps}
-                    for tb in range(kk):
-                        nx = {}
-                        for b in x:
-                            if b >> tb & 1:
-                                continue
-                            hi_ = b | (1 << tb)
-                            a_, b_ = em.tmp("p"), em.tmp("p")
-                            L(f"const float2 {a_} = __fadd2_rn({x[b]}, {x[hi_]});")
-                            L(f"const float2 {b_} = __fadd2_rn({x[b]}, {neg2(x[hi_])});")
-                            nx[b], nx[hi_] = a_, b_
-                        x = nx
-                    for P, k_ in syms.items():
-                        sv[k_] = x[P]
-                else:
-                    for P, k_ in syms.items():
-                        expr = None
-                        for sign, j in f.mixes[k_]:
-                            term = C[j] if sign > 0 else neg2(C[j])
-                            if expr is None:
-                                expr = term
-                            else:
-                                nm = em.tmp("p")
-                                L(f"const float2 {nm} = __fadd2_rn({expr}, {term});")
-                                expr = nm
-                        sv[k_] = expr
-            val = em.tree2(sym_trees[i], vv, sv)
-            gr = None
-            if want_grad:
-                gr = [em.tree2(sym_gtrees[i][a], vv, sv) if sym_gtrees[i][a] is not None
-                      else "make_float2(0.f, 0.f)" for a in range(s)]
-            return val, gr
 
         for l in range(M):
             L(f"{{  // coset {l} (packed)")
