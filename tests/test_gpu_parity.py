@@ -45,7 +45,7 @@ def _xs(z, which, dtype=torch.float32):
 
 @pytest.mark.parametrize("name", golden_names())
 @pytest.mark.parametrize("mode", ["direct", "binned", "sorted", "direct_f64", "pack2", "pack2_binned",
-                                  "radix", "radix_f64"', "presort"])
+                                  "radix", "radix_f64", "presort"])
 def test_selection_bit_exact(name, mode):
     space, _, z, arrays = load_golden(name)
     if _big(space) and mode not in ("sorted", "radix", "radix_f64", "presort"):
