@@ -92,3 +92,17 @@ def test_render_kernel_generates_and_compiles(name, shade, variant):
     _, key = compile_source(prog.source)
     spills = [int(v) for v in re.findall(r"(\d+) bytes spill stores", ptxas_info(key))]
     assert spills and max(spills) == 0
+
+
+@pytest.mark.parametrize("name", ["bcc_voronoi3", "fcc_voronoi3"])
+def test_sorted_per_polynomial_stencils_use_affine_offsets(name):
+    """Per-polynomial stencils (order-3 Voronoi) in sorted mode: each psi arm computes its
+    sites' fetch offsets from its own reference stencil and the sub-region's 4-int affine
+    record (`sg_aff0`), not from a per-site offset table; `fetch_offsets="table"` keeps the
+    table.  Both kernels are parity-tested on the GPU (test_gpu_parity)."""
+    space, _, _, arrays = load_golden(name)
+    ext = arrays[0].shape
+    a = generate(space, _cfg(space, dict(mode="sorted", radix=1)), ext)
+    b = generate(space, _cfg(space, dict(mode="sorted", radix=1, fetch_offsets="table")), ext)
+    assert a.meta["fetch_mode"] == "paffine" and "sg_aff0" in a.source and "sg_off0" not in a.source
+    assert b.meta["fetch_mode"] == "table" and "sg_off0" in b.source

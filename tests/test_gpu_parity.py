@@ -108,6 +108,7 @@ CONFIGS = [
     dict(mode="sorted", coeffs="table", tloop=1),
     dict(mode="sorted", coeffs="table", tloop=1, tpairs=2, block=256, radix=1),
     dict(coeffs="table", tloop=1),
+    dict(mode="sorted", radix=1, fetch_offsets="table"),
 ]
 
 
