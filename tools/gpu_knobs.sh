@@ -19,9 +19,11 @@ cap c2 table
 cap c2 binned_l1; cap c2 direct
 # Voronoi dispatch: predicated direct vs psi-sorted (order-2 BCC Voronoi, rays)
 cap c3o2 direct; cap c3o2 srt_imm
+# sorted-mode fetch offsets: per-polynomial affine vs per-site offset table (order-3 BCC Voronoi)
+cap c3 default; cap c3 offt_table
 for k in "dispatch:c4_c4_direct_b128 c4_c4_branchy" "form:c2_horner c2_default" \
          "coeffs:c2_default c2_table" "fetch:c2_default c2_binned_l1 c2_direct" \
-         "voronoi_dispatch:c3o2_direct c3o2_srt_imm"; do
+         "voronoi_dispatch:c3o2_direct c3o2_srt_imm" "fetch_offsets:c3_default c3_offt_table"; do
   name=${k%%:*}; reps=""
   for v in ${k#*:}; do reps="$reps gpurun_out/knob_${TAG}_$v.ncu-rep"; done
   python tools/ncu_summary.py --table $reps > gpurun_out/${TAG}_knob_${name}.txt 2>&1

@@ -226,6 +226,7 @@ VARIANTS = {
     "cm3_tl_b640_t1920": dict(coeffs="table", tloop=1, cmajor=3, block=640, tile=1920, min_blocks=1),
     "cm3_tl_b512_t2048_c42": dict(coeffs="table", tloop=1, cmajor=3, block=512, tile=2048, min_blocks=1, tchunk=42),
     "tl_b512_t2048": dict(coeffs="table", tloop=1, cmajor=0, block=512, tile=2048, min_blocks=1),
+    "offt_table": dict(fetch_offsets="table"),
     "l1_bin32_imm": dict(mode="binned", stage="l1", block=256, bin=32, coeffs="imm", branchy=True),
     "l1_bin32_table": dict(mode="binned", stage="l1", block=256, bin=32, coeffs="table"),
 }
