@@ -481,7 +481,17 @@ __global__ void __launch_bounds__(SG_SORT_THREADS) sg_bin_scatter(
 
 // K3': tile-local counting sort before the scatter: records of one bin leave the CTA as
 // contiguous runs (coalesced 16-B stores) instead of one scattered store per query.
-constexpr int SG_TILED_MAX_BINS = 2048;   // per-tile histogram cost grows with the bin count
+constexpr int SG_TILED_MAX_BINS_CAP = 10240;   // smem: 4 ints per bin + the tile's records
+// per-tile histogram cost grows with the bin count: the tiled scatter is used up to this many
+// bins (env SPLINEGPU_TILED_MAX_BINS, at most SG_TILED_MAX_BINS_CAP), the plain one above
+static int sg_tiled_max_bins() {
+  static const int v = [] {
+    const char* e = getenv("SPLINEGPU_TILED_MAX_BINS");
+    const int x = e ? atoi(e) : 2048;
+    return x >= 0 && x <= SG_TILED_MAX_BINS_CAP ? x : 2048;
+  }();
+  return v;
+}
 
 template <int THREADS, int GROUPS>
 __global__ void __launch_bounds__(THREADS) sg_bin_scatter_tiled(
@@ -1080,17 +1090,18 @@ static int sort_queries(sg_module* m, const void* xs, int64_t n, cudaStream_t st
                          2 * SG_SMEM_BINS * sizeof(int));
     cudaFuncSetAttribute(sg_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          SG_SMEM_BINS * sizeof(int));
-    const int tb = 4 * SG_TILED_MAX_BINS * sizeof(int);
-    cudaFuncSetAttribute(sg_bin_scatter_tiled<1024, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         4096 * (sizeof(float4) + sizeof(int)) + tb);
-    cudaFuncSetAttribute(sg_bin_scatter_tiled<512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         2048 * (sizeof(float4) + sizeof(int)) + tb);
-    cudaFuncSetAttribute(sg_bin_scatter_tiled<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         4096 * (sizeof(float4) + sizeof(int)) + tb);
-    cudaFuncSetAttribute(sg_bin_scatter_tiled<256, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         1024 * (sizeof(float4) + sizeof(int)) + tb);
-    cudaFuncSetAttribute(sg_bin_scatter_tiled<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         4096 * (sizeof(float4) + sizeof(int)) + tb);
+    const int tb = 4 * sg_tiled_max_bins() * sizeof(int);
+    const int cap = 227 * 1024;
+    auto attr = [&](const void* f, int recs) {
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           std::min(cap, recs * (int)(sizeof(float4) + sizeof(int)) + tb));
+    };
+    attr((const void*)sg_bin_scatter_tiled<1024, 1>, 4096);
+    attr((const void*)sg_bin_scatter_tiled<512, 1>, 2048);
+    attr((const void*)sg_bin_scatter_tiled<512, 2>, 4096);
+    attr((const void*)sg_bin_scatter_tiled<256, 1>, 1024);
+    attr((const void*)sg_bin_scatter_tiled<256, 4>, 4096);
+    cudaGetLastError();   // an attribute the device refuses shows up at launch, not here
   });
   sg_bin_count<<<(unsigned)G, SG_SORT_THREADS, nb * sizeof(int), st>>>((const float*)xs, (long long)n,
                                                                       per, g, mat, bin_tot);
@@ -1098,9 +1109,9 @@ static int sort_queries(sg_module* m, const void* xs, int64_t n, cudaStream_t st
   sg_bin_plan<<<1, 1024, 0, st>>>(bin_tot, (int)nb, (long long)n, chunk, starts, cursor, items,
                                   (int)max_items);
   CU(cudaGetLastError());
-  if (nb <= (size_t)SG_TILED_MAX_BINS) {
-    const size_t shb = 4 * scatter_threads * scatter_groups * (sizeof(float4) + sizeof(int)) +
-                       4 * nb * sizeof(int);
+  const size_t shb = 4 * scatter_threads * scatter_groups * (sizeof(float4) + sizeof(int)) +
+                     4 * nb * sizeof(int);
+  if (nb <= (size_t)sg_tiled_max_bins() && shb <= 227 * 1024) {
     const float* xq = (const float*)xs;
     if (scatter_threads == 256 && scatter_groups == 4)
       sg_bin_scatter_tiled<256, 4><<<(unsigned)G, 256, shb, st>>>(xq, (long long)n, per, g, mat, cursor, sorted);

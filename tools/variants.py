@@ -227,6 +227,13 @@ VARIANTS = {
     "cm3_tl_b512_t2048_c42": dict(coeffs="table", tloop=1, cmajor=3, block=512, tile=2048, min_blocks=1, tchunk=42),
     "tl_b512_t2048": dict(coeffs="table", tloop=1, cmajor=0, block=512, tile=2048, min_blocks=1),
     "offt_table": dict(fetch_offsets="table"),
+    "c4_bin8_b256": dict(mode="binned", block=256, bin=8),
+    "c4_bin8_b128": dict(mode="binned", block=128, bin=8),
+    "c4_bin8_b512_sym": dict(mode="binned", block=512, bin=8, form="sym"),
+    "c4_bin8_b256_sym": dict(mode="binned", block=256, bin=8, form="sym"),
+    "c4_bin8_b256_branchy": dict(mode="binned", block=256, bin=8, branchy=True),
+    "c3_sym": dict(form="sym"),
+    "c3_sites": dict(form="sites"),
     "l1_bin32_imm": dict(mode="binned", stage="l1", block=256, bin=32, coeffs="imm", branchy=True),
     "l1_bin32_table": dict(mode="binned", stage="l1", block=256, bin=32, coeffs="table"),
 }
