@@ -234,6 +234,16 @@ VARIANTS = {
     "c4_bin8_b256_branchy": dict(mode="binned", block=256, bin=8, branchy=True),
     "c3_sym": dict(form="sym"),
     "c3_sites": dict(form="sites"),
+    "t1920": dict(tile=1920),
+    "t2560": dict(tile=2560),
+    "t3840": dict(tile=3840),
+    "t4480": dict(tile=4480),
+    "b512_t4096": dict(block=512, tile=4096),
+    "b576_t4032": dict(block=576, tile=4032),
+    "b704_t3520": dict(block=704, tile=3520),
+    "radix0": dict(radix=0),
+    "radix0_smem": dict(radix=0, sigma_smem=8192),
+    "radix0_smem_t2560": dict(radix=0, sigma_smem=8192, tile=2560),
     "l1_bin32_imm": dict(mode="binned", stage="l1", block=256, bin=32, coeffs="imm", branchy=True),
     "l1_bin32_table": dict(mode="binned", stage="l1", block=256, bin=32, coeffs="table"),
 }
