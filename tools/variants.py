@@ -244,6 +244,26 @@ VARIANTS = {
     "radix0": dict(radix=0),
     "radix0_smem": dict(radix=0, sigma_smem=8192),
     "radix0_smem_t2560": dict(radix=0, sigma_smem=8192, tile=2560),
+    "c4_table": dict(mode="direct", block=128, coeffs="table"),
+    "c4_table_b256": dict(mode="direct", block=256, coeffs="table"),
+    "c4_lut": dict(mode="direct", block=128, coeffs="lut"),
+    "c4_tloop": dict(mode="direct", block=128, coeffs="table", tloop=1),
+    "c4_sites": dict(mode="direct", block=128, form="sites"),
+    "c4_b64": dict(mode="direct", block=64),
+    "c4_b128_mb8": dict(mode="direct", block=128, min_blocks=8),
+    "v_b512_t1024": dict(block=512, tile=1024, min_blocks=1),
+    "v_b512_t1024_cm3": dict(block=512, tile=1024, min_blocks=1, cmajor=3),
+    "v_b256_t1024": dict(block=256, tile=1024, min_blocks=1),
+    "v_b256_t512": dict(block=256, tile=512),
+    "v_b384_t1152": dict(block=384, tile=1152, min_blocks=1),
+    "v_b640_t1280": dict(block=640, tile=1280, min_blocks=1),
+    "v_b512_t512_cm3": dict(block=512, tile=512, cmajor=3),
+    "v_b640_t1280_cm3": dict(block=640, tile=1280, min_blocks=1, cmajor=3),
+    "v_b640_t1280_p32": dict(block=640, tile=1280, min_blocks=1, presort=32),
+    "v_b640_t1280_p16": dict(block=640, tile=1280, min_blocks=1, presort=16),
+    "v_b704_t1408": dict(block=704, tile=1408, min_blocks=1),
+    "v_b576_t1152": dict(block=576, tile=1152, min_blocks=1),
+    "v_b640_t1280_horner": dict(block=640, tile=1280, min_blocks=1, form="horner"),
     "l1_bin32_imm": dict(mode="binned", stage="l1", block=256, bin=32, coeffs="imm", branchy=True),
     "l1_bin32_table": dict(mode="binned", stage="l1", block=256, bin=32, coeffs="table"),
 }
