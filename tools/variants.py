@@ -264,6 +264,13 @@ VARIANTS = {
     "v_b704_t1408": dict(block=704, tile=1408, min_blocks=1),
     "v_b576_t1152": dict(block=576, tile=1152, min_blocks=1),
     "v_b640_t1280_horner": dict(block=640, tile=1280, min_blocks=1, form="horner"),
+    "v4_p64": dict(presort=64),
+    "v4_p16": dict(presort=16),
+    "v4_b384": dict(block=384),
+    "v4_b512": dict(block=512),
+    "v4_b256_t768": dict(tile=768),
+    "v4_b256_t512": dict(tile=512),
+    "v4_cm3": dict(cmajor=3),
     "l1_bin32_imm": dict(mode="binned", stage="l1", block=256, bin=32, coeffs="imm", branchy=True),
     "l1_bin32_table": dict(mode="binned", stage="l1", block=256, bin=32, coeffs="table"),
 }
