@@ -1091,8 +1091,12 @@ static int sort_queries(sg_module* m, const void* xs, int64_t n, cudaStream_t st
     cudaFuncSetAttribute(sg_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          SG_SMEM_BINS * sizeof(int));
     const int tb = 4 * sg_tiled_max_bins() * sizeof(int);
-    const int cap = 227 * 1024;
+    int optin = 227 * 1024;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0);
     auto attr = [&](const void* f, int recs) {
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, f);
+      const int cap = optin - (int)fa.sharedSizeBytes;   // dynamic + static <= the opt-in limit
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            std::min(cap, recs * (int)(sizeof(float4) + sizeof(int)) + tb));
     };
@@ -1111,7 +1115,9 @@ static int sort_queries(sg_module* m, const void* xs, int64_t n, cudaStream_t st
   CU(cudaGetLastError());
   const size_t shb = 4 * scatter_threads * scatter_groups * (sizeof(float4) + sizeof(int)) +
                      4 * nb * sizeof(int);
-  if (nb <= (size_t)sg_tiled_max_bins() && shb <= 227 * 1024) {
+  int optin_now = 227 * 1024;
+  cudaDeviceGetAttribute(&optin_now, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device);
+  if (nb <= (size_t)sg_tiled_max_bins() && shb + 1024 <= (size_t)optin_now) {
     const float* xq = (const float*)xs;
     if (scatter_threads == 256 && scatter_groups == 4)
       sg_bin_scatter_tiled<256, 4><<<(unsigned)G, 256, shb, st>>>(xq, (long long)n, per, g, mat, cursor, sorted);
