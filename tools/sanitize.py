@@ -5,7 +5,8 @@
 
 Modes: direct, binned (TMA bricks + the query sort kernels), sorted (psi-sorted persistent
 tiles, class-major warp chunks), sorted_table (dynamic-smem coefficient tables, site loop,
-two pairs per thread), render (sorted ray blocks).  Each launch is checked against the
+two pairs per thread), presort_grad (locality presort + gradient, c4v's shape), render
+(sorted ray blocks).  Each launch is checked against the
 oracle so a sanitizer run also proves the launch did its work.
 """
 import sys
@@ -28,6 +29,9 @@ MODES = {
                                     min_blocks=1)),
     "sorted_table": ("bcc_voronoi3", dict(mode="sorted", radix=1, coeffs="table", tloop=1,
                                           tpairs=2, block=256)),
+    # c4v's shape: locality presort (sort kernels) + sym form + gradient, affine offsets
+    "presort_grad": ("fcc_voronoi3", dict(mode="sorted", form="sym", radix=1, presort=1, grad=True,
+                                          block=640, tile=1280, min_blocks=1)),
 }
 
 
