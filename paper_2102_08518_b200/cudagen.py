@@ -1976,6 +1976,7 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 L("} break;")
             L("}")
         elif t.K == 1:
+            sctx["cur_psi"] = 0
             accs, grads, _ = run_plan([0], "")
             L(f"acc += {accs[0]};")
             if cfg.grad:
