@@ -76,7 +76,7 @@ CONFIGS = {
     "c4v": dict(space="fcc_voronoi3", extents=(161, 161, 161), queries=1 << 26, kind="uniform",
                  grad=True, scaling="weak",
                  variant=dict(mode="sorted", coeffs="imm", form="sym", block=640, tile=1280, min_blocks=1,
-                              radix=1, presort=64),
+                              radix=1, presort=64, qhoist=1),
                  desc="FCC Voronoi spline (order 3, the paper's FCC case), 4x161^3, 2^26 uniform, "
                       "value + gradient"),
     "c4v4": dict(space="fcc_voronoi4", extents=(161, 161, 161), queries=1 << 26, kind="uniform",

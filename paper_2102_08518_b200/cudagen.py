@@ -79,6 +79,8 @@ class GenConfig:
     tchunk: int = 0              # table + tloop: monomials per pass (0 = all up to 96, else 80)
     cmajor: int = 0              # sorted: evaluate class by class (1; 2 = with a CTA barrier between
                                  # classes) so the warps of an SM execute one polynomial's code
+    qhoist: int = 0              # sorted: issue all of a thread's tile query loads before the
+                                 # first selection (one memory latency per tile, not per query)
     tloop: int = 0               # coeffs="table": 1 = a runtime loop over the stencil sites (code
                                  # shared by every reference polynomial: no instruction-cache
                                  # pressure for large polynomials), 0 = fully unrolled
@@ -2192,6 +2194,18 @@ def generate(space, config: GenConfig | None = None, extents=None,
         TQ, Bk = cfg.tile, cfg.block
         PQ = TQ // Bk
         sctx["TQ"] = TQ
+        hoist = cfg.qhoist and not render
+        if hoist:
+            # every query load of this thread's share of the tile is issued before the first
+            # selection: one memory latency per tile instead of one per query
+            for r in range(PQ):
+                if presort:
+                    body.append(f"    const float4 hq{r}_ = {ldf}(reinterpret_cast<const float4*>(xs) + "
+                                f"min(q0 + {r * Bk} + (long long)threadIdx.x, n - 1));")
+                else:
+                    for d in range(s):
+                        body.append(f"    const float hq{r}_{d} = {ldf}(&xs[min(q0 + {r * Bk} + "
+                                    f"(long long)threadIdx.x, n - 1) * {s} + {d}]);")
         for r in range(PQ):
             body.append(f"    {{  // query {r} of this thread in the tile")
             body.append(f"    const int ql = {r * Bk} + (int)threadIdx.x;")
@@ -2212,7 +2226,10 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 # spatially close, so the coefficient gathers stay in L1/L2
                 body.append("    const long long qs_ = q0 + ql;")
                 body.append("    const bool valid = qs_ < n;")
-                body.append(f"    const float4 r4_ = {ldf}(reinterpret_cast<const float4*>(xs) + (valid ? qs_ : n - 1));")
+                if hoist:
+                    body.append(f"    const float4 r4_ = hq{r}_;")
+                else:
+                    body.append(f"    const float4 r4_ = {ldf}(reinterpret_cast<const float4*>(xs) + (valid ? qs_ : n - 1));")
                 body.append("    const long long qi = (long long)__float_as_int(r4_.w);")
                 body.append("    if (valid) sg_qidx[ql] = (int)qi;")
                 for d in range(s):
@@ -2223,11 +2240,12 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 body.append("    const bool valid = qi < n;")
                 body.append("    const long long qc = valid ? qi : n - 1;")
             for d in range(s if not (render or presort) else 0):
+                ld_ = f"hq{r}_{d}" if hoist else f"{ldf}(&xs[qc * {s} + {d}])"
                 if intsel:
-                    body.append(f"    const float xq{d} = {ldf}(&xs[qc * {s} + {d}]);")
+                    body.append(f"    const float xq{d} = {ld_};")
                     body.append(f"    const double x{d} = (double)xq{d};")
                 else:
-                    body.append(f"    const double x{d} = (double){ldf}(&xs[qc * {s} + {d}]);")
+                    body.append(f"    const double x{d} = (double){ld_};")
             if intsel:
                 body.extend("    " + ln for ln in int_prelude())
             sctx["r"] = r

@@ -271,6 +271,9 @@ VARIANTS = {
     "v4_b256_t768": dict(tile=768),
     "v4_b256_t512": dict(tile=512),
     "v4_cm3": dict(cmajor=3),
+    "qh": dict(qhoist=1),
+    "qh_t2560": dict(qhoist=1, tile=2560),
+    "qh_t3840": dict(qhoist=1, tile=3840),
     "l1_bin32_imm": dict(mode="binned", stage="l1", block=256, bin=32, coeffs="imm", branchy=True),
     "l1_bin32_table": dict(mode="binned", stage="l1", block=256, bin=32, coeffs="table"),
 }
