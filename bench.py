@@ -82,7 +82,7 @@ CONFIGS = {
     "c4v4": dict(space="fcc_voronoi4", extents=(161, 161, 161), queries=1 << 26, kind="uniform",
                  grad=True, scaling="weak",
                  variant=dict(mode="sorted", coeffs="table", tloop=1, tchunk=112, block=384, radix=1,
-                              presort=32),
+                              presort=32, qhoist=1),
                  desc="FCC Voronoi spline (order 4, 'cubic'), 4x161^3, 2^26 uniform, value + gradient"),
     "c5u": dict(space="bcc_voronoi3", extents=(406, 406, 406), queries=1 << 30, kind="uniform",
                 grad=False, scaling="strong", steps=20,
