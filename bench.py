@@ -548,10 +548,10 @@ def run_ours(args, rank, world, device):
     e2e_steps = max(3, min(args.steps, 20))
     lib = runtime.lib()
 
-    # 2^21-query chunks (the library default): H2D, kernel and D2H overlap on 3 streams;
-    # measured on B200 (tools/e2e_chunks.py): c2 4.11 G/s at 2^21 vs 3.92 at 2^22 and 3.04 at
-    # 2^24; much smaller chunks lose to per-call fixed work (c1 at 2^18: 1.3 vs 1.8)
-    host_chunk = 1 << 21
+    # the library's default chunk (2^21 queries, at least 4 chunks down to 2^18): H2D, kernel
+    # and D2H overlap on 3 streams; measured on B200 (tools/e2e_chunks.py, round 2): c2 4.17
+    # G/s at 2^21 vs 3.96 at 2^22, c3 4.24 at 2^21, c1 (2^20 queries) 2.84 at 2^18 vs 2.57 at 2^20
+    host_chunk = min(1 << 21, max(1 << 18, n // 4))   # the C ABI's default chunk rule
 
     def host_step():
         runtime._check(lib.sg_eval_host(ev.module.handle, ev.volume.handle,

@@ -24,7 +24,7 @@ xh = xs.cpu().pin_memory()
 oh = torch.empty(n, dtype=torch.float32).pin_memory()
 gh = torch.empty((n, space.dim), dtype=torch.float32).pin_memory() if prog.has_grad else None
 lib = runtime.lib()
-for lg in (20, 21, 22, 23, 24):
+for lg in [int(v) for v in (sys.argv[2].split(",") if len(sys.argv) > 2 else "20,21,22,23,24".split(","))]:
     chunk = 1 << lg
 
     def step():
