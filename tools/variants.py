@@ -274,6 +274,14 @@ VARIANTS = {
     "qh": dict(qhoist=1),
     "qh_t2560": dict(qhoist=1, tile=2560),
     "qh_t3840": dict(qhoist=1, tile=3840),
+    "c4_v4shape": dict(mode="sorted", coeffs="imm", form="sym", block=640, tile=1280, min_blocks=1,
+                       radix=1, presort=64, qhoist=1),
+    "c4_v4shape_nopre": dict(mode="sorted", coeffs="imm", form="sym", block=640, tile=1280,
+                             min_blocks=1, radix=1, qhoist=1),
+    "c4_v4shape_horner": dict(mode="sorted", coeffs="imm", block=640, tile=1280, min_blocks=1,
+                              radix=1, presort=64, qhoist=1),
+    "c4_v4shape_cm3": dict(mode="sorted", coeffs="imm", form="sym", block=640, tile=1280, min_blocks=1,
+                           radix=1, presort=64, qhoist=1, cmajor=3),
     "l1_bin32_imm": dict(mode="binned", stage="l1", block=256, bin=32, coeffs="imm", branchy=True),
     "l1_bin32_table": dict(mode="binned", stage="l1", block=256, bin=32, coeffs="table"),
 }
