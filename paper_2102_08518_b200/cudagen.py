@@ -202,11 +202,16 @@ def _solve_affine(ref, sten, s):
         if len(basis) == s:
             break
     if len(basis) < s:
-        # degenerate stencil (e.g. n <= s): only translations are tried
-        b = tuple(sten[0][d] - ref[0][d] for d in range(s))
-        A = exact.eye(s)
-        if all(tuple(ref[j][d] + b[d] for d in range(s)) == tuple(sten[j]) for j in range(n)):
-            return [[int(v) for v in row] for row in A], list(b)
+        # degenerate stencil (e.g. n <= s, or coplanar sites): A is not determined by the
+        # sites, so the signed permutations (the producer's symmetry maps) are tried
+        import itertools as _it
+        for perm in _it.permutations(range(s)):
+            for signs in _it.product((1, -1), repeat=s):
+                A = [[signs[i] if perm[i] == j else 0 for j in range(s)] for i in range(s)]
+                b = [sten[0][d] - sum(A[d][e] * ref[0][e] for e in range(s)) for d in range(s)]
+                if all(tuple(sum(A[d][e] * ref[j][e] for e in range(s)) + b[d] for d in range(s))
+                       == tuple(sten[j]) for j in range(n)):
+                    return A, b
         return None
     R = [[Fraction(v[d]) for (_, v) in basis] for d in range(s)]   # columns = ref diffs
     S = [[Fraction(sten[j][d] - sten[0][d]) for (j, _) in basis] for d in range(s)]
