@@ -625,7 +625,6 @@ def generate(space, config: GenConfig | None = None, extents=None,
         raise ValueError("presort applies to mode='sorted' (query kernels)")
     if presort and (s > 3 or len(set(ext)) != 1):
         raise ValueError("presort needs equal coset extents and dimension <= 3")
-
     pack2 = cfg.pack == 2
     if pack2:
         if cfg.float_width != F32 or cfg.mode not in ("direct", "binned"):
