@@ -292,8 +292,22 @@ def main():
     ap.add_argument("config", nargs="?", default="c2")
     ap.add_argument("--only", default="")
     ap.add_argument("--reps", type=int, default=50)
+    ap.add_argument("--extra", default="", help="JSON {name: overrides} added to the variant list")
+    ap.add_argument("--compile-only", action="store_true",
+                    help="compile the selected variants into the kernel cache (no GPU needed)")
     a = ap.parse_args()
+    if a.extra:
+        VARIANTS.update(json.loads(a.extra))
     c = bench.CONFIGS[a.config]
+    if a.compile_only:
+        from paper_2102_08518_b200.runtime import compile_source
+        for name, over in VARIANTS.items():
+            if a.only and name not in a.only.split(","):
+                continue
+            _, prog = bench.build_program(a.config, **over)
+            compile_source(prog.source)
+            print(f"{name:28s} compiled", flush=True)
+        return
     if c["kind"] == "render":
         return render_variants(a, c)
     dev = torch.device("cuda", 0)
