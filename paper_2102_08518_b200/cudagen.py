@@ -86,6 +86,10 @@ class GenConfig:
                                  # pressure for large polynomials), 0 = fully unrolled
     fetch_offsets: str = "affine"  # sorted mode, per-polynomial stencils: "affine" (offsets from
                                    # the arm's reference stencil + 4 ints per sub-region) | "table"
+    gtables: str = ""            # sorted / direct / render: comma-separated shared tables read
+                                 # from global memory (L1-cached __ldg) instead of being staged in
+                                 # shared memory, e.g. "sg_Tq" -- frees shared memory so the L1
+                                 # carve-out stays larger at a given tile size
     fetch: str = "point"         # "linear": hardware-filtered texture fetches for tensor-product
                                  # spaces (opt-in, ~1e-3 accurate: linfetch.py)
 
@@ -915,7 +919,16 @@ def generate(space, config: GenConfig | None = None, extents=None,
             lit = ", ".join(dlit(Fraction(v)) for v in vals)
         # global (not __constant__): the per-CTA staging copy reads thread-distinct addresses,
         # which the constant cache serializes; coalesced __ldg reads do not
-        A(f"__device__ const {ctype} {name}_c[{len(vals)}] = {{{lit}}};")
+        A(f"__device__ const __align__(16) {ctype} {name}_c[{len(vals)}] = {{{lit}}};")
+    gset = {g for g in cfg.gtables.split(",") if g}
+    if gset:
+        if cfg.mode == "binned":
+            raise ValueError("gtables applies to the sorted / direct / render kernels")
+        bad = sorted(g for g in gset if not g.startswith("sg_"))
+        if bad:   # tables a space does not have (e.g. sg_psi with one polynomial) are skipped
+            raise ValueError(f"gtables: {bad} are not shared-table names (sg_Tq, sg_aff0, ...)")
+    gtabs = [e for e in smem if e[0] in gset]
+    smem = [e for e in smem if e[0] not in gset]
 
     if radix is not None:
         A(f"__device__ const short sg_sigma_r[{len(tab_r)}] = {{{', '.join(str(v) for v in tab_r)}}};")
@@ -1046,6 +1059,8 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 B(f"  {ctype}* {name} = reinterpret_cast<{ctype}*>(sg_dyn + {off});")
         for name, ctype, vals in smem:
             B(f"  for (int i_ = threadIdx.x; i_ < {len(vals)}; i_ += {cfg.block}) {name}[i_] = __ldg(&{name}_c[i_]);")
+        for name, ctype, _vals in gtabs:
+            B(f"  const {ctype}* __restrict__ {name} = {name}_c;")
         if sorted_:
             TQ = cfg.tile
             MP = M * TQ

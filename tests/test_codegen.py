@@ -106,3 +106,22 @@ def test_sorted_per_polynomial_stencils_use_affine_offsets(name):
     b = generate(space, _cfg(space, dict(mode="sorted", radix=1, fetch_offsets="table")), ext)
     assert a.meta["fetch_mode"] == "paffine" and "sg_aff0" in a.source and "sg_off0" not in a.source
     assert b.meta["fetch_mode"] == "table" and "sg_off0" in b.source
+
+
+def test_gtables_read_selection_tables_from_global_memory():
+    """`gtables` keeps the named tables in global memory (read through L1 with __ldg) instead
+    of staging them in shared memory; the sorted kernel's shared footprint drops by their
+    bytes.  Parity of the variant is in test_gpu_parity."""
+    space, _, _, arrays = load_golden("bcc_voronoi3")
+    ext = arrays[0].shape
+    a = generate(space, _cfg(space, dict(mode="sorted", radix=1)), ext)
+    b = generate(space, _cfg(space, dict(mode="sorted", radix=1, gtables="sg_Tq,sg_psi")), ext)
+    assert "__shared__ __align__(16) float sg_Tq[" in a.source
+    assert "__shared__ __align__(16) float sg_Tq[" not in b.source
+    assert "const float* __restrict__ sg_Tq = sg_Tq_c;" in b.source
+    assert "const int* __restrict__ sg_psi = sg_psi_c;" in b.source
+    assert b.smem_bytes == a.smem_bytes          # the tile's dynamic records are unchanged
+    with pytest.raises(ValueError):
+        generate(space, _cfg(space, dict(mode="sorted", gtables="Tq")), ext)
+    with pytest.raises(ValueError):
+        generate(space, _cfg(space, dict(mode="binned", gtables="sg_Tq")), ext)
