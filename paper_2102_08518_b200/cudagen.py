@@ -86,6 +86,8 @@ class GenConfig:
                                  # pressure for large polynomials), 0 = fully unrolled
     fetch_offsets: str = "affine"  # sorted mode, per-polynomial stencils: "affine" (offsets from
                                    # the arm's reference stencil + 4 ints per sub-region) | "table"
+    cflip: int = 0               # sorted + cmajor=3: alternate the psi order tile by tile (the
+                                 # last polynomial's code is still hot when the next tile starts)
     gtables: str = ""            # sorted / direct / render: comma-separated shared tables read
                                  # from global memory (L1-cached __ldg) instead of being staged in
                                  # shared memory, e.g. "sg_Tq" -- frees shared memory so the L1
@@ -1115,11 +1117,15 @@ def generate(space, config: GenConfig | None = None, extents=None,
                 # C ABI before the launch): the resident CTAs work on a contiguous window of
                 # the query stream -- coherent L1/L2 footprint, no tail imbalance
                 B("  __shared__ long long sg_q0;")
+                if cfg.cflip:
+                    B("  int sg_par = 1;")
                 B("  for (;;) {")
                 B(f"  if (threadIdx.x == 0) sg_q0 = (long long)atomicAdd(err + 1, 1u) * {TQ};")
                 B("  __syncthreads();")
                 B("  const long long q0 = sg_q0;")
                 B("  if (q0 >= n) break;")
+                if cfg.cflip:
+                    B("  sg_par ^= 1;")
         elif smem:
             B("  __syncthreads();")
         if sorted_:
@@ -2386,8 +2392,14 @@ def generate(space, config: GenConfig | None = None, extents=None,
             body.append("      if (lane == 0) ch_ = atomicAdd(&sg_next, 1);")
             body.append("      ch_ = __shfl_sync(0xffffffffu, ch_, 0);")
             body.append("      if (ch_ * 32 >= tot) break;")
-            body.append("      const int pos = ch_ * 32 + (int)lane;")
-            body.append("      if (pos >= tot) continue;")
+            if cfg.cflip and not render:
+                # odd tiles walk the psi order backwards (chunks stay contiguous runs)
+                body.append("      const int r_ = ch_ * 32 + (int)lane;")
+                body.append("      if (r_ >= tot) continue;")
+                body.append("      const int pos = sg_par ? tot - 1 - r_ : r_;")
+            else:
+                body.append("      const int pos = ch_ * 32 + (int)lane;")
+                body.append("      if (pos >= tot) continue;")
             body.append("      const int e_ = sg_ord[pos];")
             body.append("      const int pi_ = e_ & 0xffff;")
             body.append("      const int sub = e_ >> 16;")
