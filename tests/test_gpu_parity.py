@@ -110,6 +110,7 @@ CONFIGS = [
     dict(coeffs="table", tloop=1),
     dict(mode="sorted", radix=1, fetch_offsets="table"),
     dict(mode="sorted", radix=1, gtables="sg_Tq,sg_aff0,sg_off0,sg_psi,sg_sigma"),
+    dict(mode="sorted", radix=1, cmajor=3, cflip=1, tile=256, block=128),
     dict(mode="sorted", radix=1, qhoist=1, tile=512, block=128),
     dict(mode="sorted", radix=1, qhoist=1, presort=4, tile=512, block=128),
 ]
