@@ -125,3 +125,15 @@ def test_gtables_read_selection_tables_from_global_memory():
         generate(space, _cfg(space, dict(mode="sorted", gtables="Tq")), ext)
     with pytest.raises(ValueError):
         generate(space, _cfg(space, dict(mode="binned", gtables="sg_Tq")), ext)
+
+
+def test_cflip_alternates_the_class_order_per_tile():
+    """`cflip` (sorted mode, cmajor=3): every other tile walks its psi-ordered pairs backwards;
+    without class-major chunks the knob has no effect.  Parity in test_gpu_parity."""
+    space, _, _, arrays = load_golden("bcc_voronoi3")
+    ext = arrays[0].shape
+    a = generate(space, _cfg(space, dict(mode="sorted", radix=1, cmajor=3, cflip=1)), ext)
+    assert "int sg_par = 1;" in a.source and "sg_par ^= 1;" in a.source
+    assert "const int pos = sg_par ? tot - 1 - r_ : r_;" in a.source
+    b = generate(space, _cfg(space, dict(mode="sorted", radix=1, cmajor=3)), ext)
+    assert "sg_par" not in b.source
